@@ -1,0 +1,38 @@
+"""B200-native point-cloud sampling: FPS, AFPS and NPDU-AFPS (arXiv 2208.08795).
+
+Two faces over the same sm_100a kernels (C-ABI: include/pcs_gpu.h):
+
+* the reference's Python API, ``pcsample._core`` compatible
+  (proj/bindings/pcsample_module.cpp:122-190): ``fps``, ``afps``,
+  ``npdu_fps``, ``npdu_afps``, ``exact_sort`` (and ``local_fps`` with the
+  DistanceTrace) taking float64 ``(N, 3)`` arrays and returning
+  ``(int64 idx, int64 sector_of, stats dict)``;
+* a batched, stream-ordered torch op, :func:`sample` / :func:`sort_axis`,
+  taking CUDA tensors ``(B, N, 3)`` and returning ``int32 (B, C)`` indices plus
+  ``(B, 4)`` OpStats, capturable in CUDA graphs.
+
+There is no CPU fallback: importing without the built extension raises.
+"""
+from __future__ import annotations
+
+import os as _os
+
+_PKG = _os.path.dirname(_os.path.abspath(__file__))
+
+try:
+    from . import _core  # noqa: F401  (loads lib/libpcs_gpu.so)
+except ImportError as exc:  # pragma: no cover - exercised only when unbuilt
+    raise ImportError(
+        "paper_2208_08795_b200: native extension not built "
+        "(run `python -m paper_2208_08795_b200._build`); there is no CPU fallback"
+    ) from exc
+
+from ._core import afps, exact_sort, fps, local_fps, npdu_afps, npdu_fps  # noqa: E402
+from .ops import METHODS, sample, sort_axis, sample_host_batch  # noqa: E402
+
+LIB_PATH = _os.path.join(_PKG, "lib", "libpcs_gpu.so")
+
+__all__ = [
+    "fps", "afps", "npdu_fps", "npdu_afps", "exact_sort", "local_fps",
+    "sample", "sort_axis", "sample_host_batch", "METHODS", "LIB_PATH",
+]

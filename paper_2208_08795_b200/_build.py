@@ -1,0 +1,91 @@
+"""In-tree build of the native pieces (no GPU needed; nvcc cross-compiles).
+
+    python -m paper_2208_08795_b200._build        # or __graft_entry__.build()
+
+Outputs (git-ignored, shipped to the GPU box by gpurun's snapshot):
+  paper_2208_08795_b200/lib/libpcs_gpu.so  -- sm_100a kernels + C-ABI
+                                              (include/pcs_gpu.h) + the C++
+                                              drop-in namespace pcs
+  paper_2208_08795_b200/_core*.so          -- pybind11 module over the drop-in
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+LIBDIR = os.path.join(PKG, "lib")
+OBJDIR = os.path.join(PKG, "build")
+LIB = os.path.join(LIBDIR, "libpcs_gpu.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CU_SRCS = ["sample_kernels.cu", "sort_kernels.cu"]
+CXX_SRCS = ["capi.cpp", "pcs_api.cpp"]
+HEADERS = ["device_common.cuh", "internal.h"]
+
+
+def core_path():
+    return os.path.join(PKG, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _headers():
+    hs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INC, "pcs_gpu.h")]
+    hs += [os.path.join(INC, "pcs", f) for f in os.listdir(os.path.join(INC, "pcs"))]
+    return hs
+
+
+def build(verbose=False):
+    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
+    hdrs = _headers()
+    objs = []
+    for src in CU_SRCS:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJDIR, src + ".o")
+        objs.append(o)
+        if _newer(o, [s] + hdrs):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xptxas", "-warn-spills", "-I", INC, "-c", s, "-o", o], verbose)
+    for src in CXX_SRCS:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJDIR, src + ".o")
+        objs.append(o)
+        if _newer(o, [s] + hdrs):
+            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-I", INC,
+                  "-I", os.path.join(CUDA, "include"), "-c", s, "-o", o], verbose)
+    if _newer(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs], verbose)
+    core = core_path()
+    mod_src = os.path.join(CSRC, "pybind_module.cpp")
+    if _newer(core, [mod_src, LIB] + hdrs):
+        import pybind11
+
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", INC,
+              "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"],
+              mod_src, "-o", core, "-L", LIBDIR, "-lpcs_gpu", "-Wl,-rpath,$ORIGIN/lib"],
+             verbose)
+    return LIB, core
+
+
+if __name__ == "__main__":
+    build(verbose="-q" not in sys.argv)

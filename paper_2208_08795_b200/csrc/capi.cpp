@@ -1,0 +1,255 @@
+// C-ABI entry points (include/pcs_gpu.h): host-side validation in the
+// reference's order, error plumbing, and the host-buffer drop-ins that the
+// reference-facing bindings call.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+#include "pcs_gpu.h"
+
+namespace pcs_internal {
+namespace {
+thread_local std::string g_error;
+
+const char* who(int method) {
+  switch (method) {
+    case PCS_METHOD_FPS: return "fps";
+    case PCS_METHOD_AFPS: return "afps";
+    case PCS_METHOD_NPDU_FPS: return "npdu_fps";
+    case PCS_METHOD_NPDU_AFPS: return "npdu_afps";
+  }
+  return "run_sampler";
+}
+
+int cuda_fail(cudaError_t e, const std::string& extra = "") {
+  if (e == cudaErrorNotSupported && !extra.empty()) {
+    set_error(extra);
+    return PCS_ERR_UNSUPPORTED;
+  }
+  set_error(std::string("CUDA error: ") + cudaGetErrorString(e) + (extra.empty() ? "" : " (" + extra + ")"));
+  return PCS_ERR_CUDA;
+}
+
+// RAII device buffer on a stream (stream-ordered allocator).
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit DevBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 16, s); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+void clear_error() { g_error.clear(); }
+
+int validate_sample(int method, int64_t n, int64_t c, int64_t m, int64_t k, std::string* msg) {
+  if (method < PCS_METHOD_FPS || method > PCS_METHOD_NPDU_AFPS) {
+    *msg = "run_sampler: unknown method";
+    return PCS_ERR_INVALID_ARGUMENT;
+  }
+  const std::string w = who(method);
+  // check_sample_count, proj/src/sampler.cpp:20-23
+  if (c < 1) { *msg = w + ": c must be >= 1"; return PCS_ERR_INVALID_ARGUMENT; }
+  if (c > n) { *msg = w + ": c exceeds point count"; return PCS_ERR_INVALID_ARGUMENT; }
+  const bool sectored = method == PCS_METHOD_AFPS || method == PCS_METHOD_NPDU_AFPS;
+  if (sectored) {
+    // SectorPlan::make -> partition_sectors -> allocate_samples -> feasibility,
+    // proj/src/sectors.cpp:9-51
+    if (m < 1) { *msg = "partition_sectors: m must be >= 1"; return PCS_ERR_INVALID_ARGUMENT; }
+    if (m > n) { *msg = "partition_sectors: m exceeds point count"; return PCS_ERR_INVALID_ARGUMENT; }
+    if (m > c) { *msg = "allocate_samples: m exceeds sample count"; return PCS_ERR_INVALID_ARGUMENT; }
+    // First infeasible sector, if any: sizes nb+[s<nr], quotas cb+[s<cr].
+    const int64_t nb = n / m, nr = n % m, cb = c / m, cr = c % m;
+    int64_t bad = -1;
+    if (cb > nb) bad = 0;
+    else if (cb == nb && cr > nr) bad = nr;
+    if (bad >= 0) {
+      *msg = "sector " + std::to_string(bad) + " holds " + std::to_string(nb + (bad < nr)) +
+             " points but owes " + std::to_string(cb + (bad < cr)) + " samples";
+      return PCS_ERR_INVALID_ARGUMENT;
+    }
+  }
+  // local_fps, proj/src/sampler.cpp:89-94 (range and quota hold by now)
+  const bool windowed = method == PCS_METHOD_NPDU_FPS || method == PCS_METHOD_NPDU_AFPS;
+  if (windowed && k < 1) { *msg = "local_fps: window size must be >= 1"; return PCS_ERR_INVALID_ARGUMENT; }
+  if (n > 0x7fffffffLL) { *msg = "clouds above 2^31-1 points are not supported"; return PCS_ERR_UNSUPPORTED; }
+  return PCS_OK;
+}
+
+}  // namespace pcs_internal
+
+using namespace pcs_internal;
+
+extern "C" {
+
+int pcs_abi_version(void) { return PCS_GPU_ABI_VERSION; }
+
+const char* pcs_last_error(void) { return g_error.c_str(); }
+
+const char* pcs_status_string(int status) {
+  switch (status) {
+    case PCS_OK: return "ok";
+    case PCS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case PCS_ERR_CUDA: return "CUDA error";
+    case PCS_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+int pcs_gpu_sample(const pcs_gpu_args* a, void* stream) {
+  clear_error();
+  if (!a) { set_error("pcs_gpu_sample: null args"); return PCS_ERR_INVALID_ARGUMENT; }
+  std::string msg;
+  const int rc = validate_sample(a->method, a->n, a->c, a->m, a->k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  if (a->batch < 0) { set_error("pcs_gpu_sample: batch must be >= 0"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (a->batch == 0) return PCS_OK;
+  if (!a->xyz || !a->out_indices) { set_error("pcs_gpu_sample: null buffer"); return PCS_ERR_INVALID_ARGUMENT; }
+  const cudaError_t e = launch_sample(*a, static_cast<cudaStream_t>(stream), &msg);
+  return e == cudaSuccess ? PCS_OK : cuda_fail(e, msg);
+}
+
+int pcs_gpu_sort_axis(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                      int32_t axis, void* out_xyz, int32_t* out_perm, void* stream) {
+  clear_error();
+  if (axis < 0 || axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (n > 0x7fffffffLL) { set_error("clouds above 2^31-1 points are not supported"); return PCS_ERR_UNSUPPORTED; }
+  const cudaError_t e = launch_sort(coord_dtype, xyz, batch, n, axis, out_xyz, out_perm,
+                                    static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PCS_OK : cuda_fail(e);
+}
+
+int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int64_t m,
+                    int64_t k, int32_t seed_policy, uint64_t seed, uint32_t threads,
+                    int64_t* out_indices, int64_t* out_sector, uint64_t* out_stats) {
+  (void)threads;  // accepted for pcs::afps(..., threads) parity; GPU schedule is fixed
+  clear_error();
+  std::string msg;
+  int rc = validate_sample(method, n, c, m, k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  {
+    DevBuf dx(st), didx(st), dsec(st), dstat(st);
+    if ((e = dx.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
+        (e = didx.alloc(sizeof(int64_t) * c)) != cudaSuccess ||
+        (e = dsec.alloc(sizeof(int32_t) * c)) != cudaSuccess ||
+        (e = dstat.alloc(sizeof(uint64_t) * 4)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dx.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+      rc = cuda_fail(e);
+    } else {
+      pcs_gpu_args a{};
+      a.method = method;
+      a.coord_dtype = PCS_DTYPE_F64;
+      a.xyz = dx.p;
+      a.batch = 1;
+      a.n = n;
+      a.c = c;
+      a.m = m;
+      a.k = k;
+      a.seed_policy = seed_policy;
+      a.seed = seed;
+      a.index_dtype = PCS_INDEX_I64;
+      a.out_indices = didx.p;
+      a.out_sector = static_cast<int32_t*>(dsec.p);
+      a.out_stats = static_cast<uint64_t*>(dstat.p);
+      e = launch_sample(a, st, &msg);
+      if (e != cudaSuccess) {
+        rc = cuda_fail(e, msg);
+      } else {
+        int32_t* sec32 = new int32_t[c];
+        if ((e = cudaMemcpyAsync(out_indices, didx.p, sizeof(int64_t) * c, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(sec32, dsec.p, sizeof(int32_t) * c, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(out_stats, dstat.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+          rc = cuda_fail(e);
+        } else if (out_sector) {
+          for (int64_t i = 0; i < c; ++i) out_sector[i] = sec32[i];
+        }
+        delete[] sec32;
+      }
+    }
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int pcs_local_fps_host(const double* xyz, int64_t n, int64_t sb, int64_t se, int64_t quota,
+                       int64_t k, int32_t seed_policy, uint64_t seed, int64_t* out_indices,
+                       uint64_t* out_stats, double* trace) {
+  clear_error();
+  // proj/src/sampler.cpp:89-94, same order and messages.
+  if (se > n || sb < 0 || sb >= se) { set_error("local_fps: sector out of range"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (quota < 1 || quota > se - sb) { set_error("local_fps: quota infeasible for sector"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (k == 0) { set_error("local_fps: window size must be >= 1"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (n > 0x7fffffffLL) { set_error("clouds above 2^31-1 points are not supported"); return PCS_ERR_UNSUPPORTED; }
+  // k < 0 encodes std::nullopt (full window).
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int rc = PCS_OK;
+  const int64_t len = se - sb;
+  {
+    DevBuf dx(st), didx(st), dstat(st), dtr(st);
+    const size_t trace_n = trace ? static_cast<size_t>(quota > 1 ? quota - 1 : 0) * len : 0;
+    std::string msg;
+    if ((e = dx.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
+        (e = didx.alloc(sizeof(int64_t) * quota)) != cudaSuccess ||
+        (e = dstat.alloc(sizeof(uint64_t) * 4)) != cudaSuccess ||
+        (trace && (e = dtr.alloc(sizeof(double) * trace_n)) != cudaSuccess) ||
+        (e = cudaMemcpyAsync(dx.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = launch_local_fps(static_cast<double*>(dx.p), n, sb, se, quota, k < 0 ? 0 : k,
+                              seed_policy == PCS_RANDOM_FIRST_POINT, seed,
+                              static_cast<int64_t*>(didx.p), static_cast<uint64_t*>(dstat.p),
+                              trace ? static_cast<double*>(dtr.p) : nullptr, st, &msg)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(out_indices, didx.p, sizeof(int64_t) * quota, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(out_stats, dstat.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (trace && trace_n && (e = cudaMemcpyAsync(trace, dtr.p, sizeof(double) * trace_n, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+      rc = cuda_fail(e, msg);
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_xyz,
+                        int64_t* out_perm) {
+  clear_error();
+  if (axis < 0 || axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (n <= 0) return PCS_OK;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int rc = PCS_OK;
+  {
+    DevBuf dx(st), dout(st), dperm(st);
+    int32_t* perm32 = new int32_t[n];
+    if ((e = dx.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
+        (e = dout.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
+        (e = dperm.alloc(sizeof(int32_t) * n)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dx.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = launch_sort(PCS_DTYPE_F64, dx.p, 1, n, axis, dout.p, static_cast<int32_t*>(dperm.p), st)) != cudaSuccess ||
+        (out_xyz && (e = cudaMemcpyAsync(out_xyz, dout.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (e = cudaMemcpyAsync(perm32, dperm.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      rc = cuda_fail(e);
+    } else if (out_perm) {
+      for (int64_t i = 0; i < n; ++i) out_perm[i] = perm32[i];
+    }
+    delete[] perm32;
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+"""Batched torch-facing sampling op over the C-ABI (include/pcs_gpu.h).
+
+The reference samples one cloud per call (proj/include/pcs/sampler.hpp:41-66);
+PointNet++-style callers sample a whole batch per set-abstraction layer. This
+module is that batched entry: CUDA tensors in, CUDA tensors out, enqueued on
+the current torch stream, no host synchronisation, so it can sit inside a
+CUDA graph. Torch is plumbing here (device memory, streams); every FLOP runs
+in the sm_100a kernels of libpcs_gpu.so.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _core
+
+METHODS = {"fps": 1, "afps": 2, "npdu_fps": 3, "npdu_afps": 4}
+_AXES = {"x": 0, "y": 1, "z": 2, 0: 0, 1: 1, 2: 2}
+
+
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _as_batch(xyz: torch.Tensor) -> torch.Tensor:
+    if xyz.dim() == 2:
+        xyz = xyz.unsqueeze(0)
+    if xyz.dim() != 3 or xyz.shape[-1] != 3:
+        raise ValueError("expected an (N, 3) or (B, N, 3) tensor")
+    if not xyz.is_cuda:
+        raise ValueError("xyz must be a CUDA tensor (use sample_host_batch for host arrays)")
+    if xyz.dtype not in (torch.float32, torch.float64):
+        raise ValueError("xyz must be float32 or float64")
+    return xyz.contiguous()
+
+
+def sort_axis(xyz: torch.Tensor, axis="x"):
+    """Stable per-cloud sort along ``axis`` (pcs::exact_sort semantics,
+    proj/src/order.cpp:11-24). Returns ``(sorted_xyz, perm int32)`` with
+    ``sorted_xyz[b, i] == xyz[b, perm[b, i]]``."""
+    if axis not in _AXES:
+        raise ValueError("axis must be x, y, or z")
+    x = _as_batch(xyz)
+    B, N = x.shape[0], x.shape[1]
+    out = torch.empty_like(x)
+    perm = torch.empty((B, N), dtype=torch.int32, device=x.device)
+    _core.sort_device(1 if x.dtype == torch.float64 else 0, x.data_ptr(), B, N, _AXES[axis],
+                      out.data_ptr(), perm.data_ptr(), _stream_handle(x.device))
+    return out, perm
+
+
+def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optional[int] = None,
+           first: str = "fixed", seed: int = 0, seeds: Optional[torch.Tensor] = None,
+           sort: Optional[str] = None, index_dtype: torch.dtype = torch.int32,
+           return_sector: bool = False, index_base: int = 0, sector_base: int = 0):
+    """Sample ``c`` points from every cloud of ``xyz`` (CUDA, ``(B, N, 3)``).
+
+    ``method`` is one of fps / afps / npdu_fps / npdu_afps; ``m`` sectors for
+    the AFPS variants, ``k`` window for the NPDU variants (the reference's
+    ``k``; BASELINE's "w neighbours each side" is ``k = 2w + 1``). ``first``
+    is "fixed" (FixedFirstPoint) or "random" (SplitMix64(seed ^ sector)).
+    ``sort``: optional axis; clouds are first stably sorted (exact_sort) and
+    the indices then refer to the sorted clouds, exactly as
+    ``afps(exact_sort(cloud), ...)`` does in the reference.
+
+    Returns ``(indices (B, c), stats int64 (B, 4))`` plus ``sector_of``
+    (int32) when ``return_sector`` and ``perm`` (int32) when ``sort``.
+    Stats columns: dist_evals, dist_writes, argmax_scans, iterations.
+    ``index_base`` / ``sector_base`` shift output indices / sector ids when
+    the batch is a shard (a storage slice) of a larger cloud.
+    """
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    if first not in ("fixed", "random"):
+        raise ValueError("first must be 'random' or 'fixed'")
+    x = _as_batch(xyz)
+    perm = None
+    if sort is not None:
+        x, perm = sort_axis(x, sort)
+    B, N = x.shape[0], x.shape[1]
+    dev = x.device
+    if index_dtype not in (torch.int32, torch.int64):
+        raise ValueError("index_dtype must be torch.int32 or torch.int64")
+    idx = torch.empty((B, max(int(c), 0)), dtype=index_dtype, device=dev)
+    stats = torch.empty((B, 4), dtype=torch.int64, device=dev)
+    sector = torch.empty((B, max(int(c), 0)), dtype=torch.int32, device=dev) if return_sector else None
+    seeds_ptr = 0
+    if seeds is not None:
+        seeds = seeds.to(device=dev, dtype=torch.int64).contiguous()
+        if seeds.numel() != B:
+            raise ValueError("seeds must hold one seed per cloud")
+        seeds_ptr = seeds.data_ptr()
+    _core.sample_device(METHODS[method], 1 if x.dtype == torch.float64 else 0, x.data_ptr(), B, N,
+                        int(c), int(m), int(k) if k is not None else 0,
+                        1 if first == "fixed" else 0, int(seed) & (2**64 - 1), seeds_ptr,
+                        1 if index_dtype == torch.int64 else 0, idx.data_ptr(),
+                        sector.data_ptr() if sector is not None else 0, stats.data_ptr(),
+                        _stream_handle(dev), int(index_base), int(sector_base))
+    out = [idx, stats]
+    if return_sector:
+        out.append(sector)
+    if perm is not None:
+        out.append(perm)
+    return tuple(out)
+
+
+def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,
+                      k: Optional[int] = None, first: str = "fixed", seed: int = 0,
+                      sort: Optional[str] = None, device: str = "cuda"):
+    """Host (numpy) batch in, host results out: H2D copy, sample, D2H copy.
+    The end-to-end path the bench's ``e2e`` figure measures."""
+    arr = np.ascontiguousarray(xyz)
+    host = torch.from_numpy(arr).pin_memory()
+    dev = host.to(device, non_blocking=True)
+    res = sample(dev, c, method=method, m=m, k=k, first=first, seed=seed, sort=sort)
+    return tuple(t.cpu().numpy() for t in res)

@@ -1,0 +1,224 @@
+"""Parity of the CUDA path with the oracle / the real reference (GPU only).
+
+Bit-exact is the bar everywhere: sampled indices, sector_of and all four
+OpStats counters (integer work), and the DistanceTrace snapshots (fp64, same
+operation order, no FMA -> identical bits). Everything goes through the
+C-ABI: the drop-in Python surface (pcs.fps, ...) calls pcs_sample_host, the
+batched torch op calls pcs_gpu_sample / pcs_gpu_sort_axis.
+"""
+import numpy as np
+import pytest
+
+from conftest import METHOD_NAMES, load_sampler_goldens, load_sort_goldens
+from paper_2208_08795_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+LINE = np.array([[float(x), 0.0, 0.0] for x in range(8)])
+
+
+def _call(pcs, meth, pts, c, m, k, first, seed):
+    if meth == "fps":
+        return pcs.fps(pts, c, seed=seed, first=first)
+    if meth == "afps":
+        return pcs.afps(pts, c, m, seed=seed, first=first)
+    if meth == "npdu_fps":
+        return pcs.npdu_fps(pts, c, k, seed=seed, first=first)
+    return pcs.npdu_afps(pts, c, m, k, seed=seed, first=first)
+
+
+def _same(got, idx, sec, st):
+    np.testing.assert_array_equal(got[0], idx)
+    np.testing.assert_array_equal(got[1], sec)
+    assert [got[2][f] for f in ("dist_evals", "dist_writes", "argmax_scans", "iterations")] == \
+        [int(x) for x in st]
+
+
+@pytest.mark.parametrize("name", sorted(load_sampler_goldens()))
+def test_goldens_through_dropin(pcs, name):
+    g = load_sampler_goldens()[name]
+    got = _call(pcs, METHOD_NAMES[int(g["method"])], g["points"], int(g["c"]), int(g["m"]),
+                int(g["k"]), "random" if int(g["random_first"]) else "fixed", int(g["seed"]))
+    _same(got, g["indices"], g["sector_of"], g["stats"])
+
+
+def test_reference_kats(pcs):
+    # proj/tests/test_sampler.cpp:88-113, 184-220, 267-344
+    assert pcs.fps(LINE[:4], 2, first="fixed")[0].tolist() == [0, 3]
+    assert pcs.fps(LINE[:4], 3, first="fixed")[0].tolist() == [0, 3, 1]
+    assert pcs.fps(LINE[:4], 4, first="fixed")[0].tolist() == [0, 3, 1, 2]
+    idx, _, st = pcs.npdu_fps(LINE, 3, 2, first="fixed")
+    assert idx.tolist() == [0, 1, 2]
+    assert (st["dist_evals"], st["dist_writes"], st["iterations"]) == (3, 2, 2)
+    assert pcs.npdu_fps(LINE, 3, 4, first="fixed")[0].tolist() == [0, 2, 4]
+    one = pcs.fps(synth.random_cloud(100, 17), 1, first="fixed")
+    assert one[0].tolist() == [0] and set(one[2].values()) == {0}
+    r = pcs.fps(synth.random_cloud(100, 17), 25, seed=5)
+    assert r[2]["dist_evals"] == 2400 and r[2]["argmax_scans"] == 2400 and r[2]["iterations"] == 24
+    cloud = synth.random_cloud(2048, 2)
+    r = pcs.afps(cloud, 512, 32, seed=1)
+    assert r[2]["dist_evals"] == 30720 and len(set(r[0].tolist())) == 512
+    assert pcs.afps(synth.random_cloud(10, 3), 4, 3, first="fixed")[2]["dist_evals"] == 4
+    r = pcs.afps(synth.random_cloud(100, 5), 20, 20, seed=77)
+    assert r[2]["dist_evals"] == 0 and r[1].tolist() == list(range(20))
+    assert pcs.npdu_fps(synth.random_cloud(64, 4), 10, 1, seed=8)[2]["dist_evals"] == 9
+    r = pcs.npdu_afps(synth.random_cloud(2048, 6), 512, 32, 16, seed=2)
+    assert r[2]["dist_evals"] <= 7680 and len(set(r[0].tolist())) == 512
+    a = pcs.npdu_afps(synth.random_cloud(2048, 6), 512, 32, 16, seed=2, threads=4)
+    assert a[0].tolist() == r[0].tolist() and a[2] == r[2]
+
+
+def test_reduction_identities(pcs):
+    # proj/tests/acceptance_main.cpp:128-171
+    rng = np.random.default_rng(260856)
+    for trial in range(25):
+        n = int(rng.integers(16, 416))
+        c = int(rng.integers(2, n + 1))
+        m = int(rng.integers(1, c + 1))
+        k = int(rng.integers(1, 25))
+        seed = int(rng.integers(0, 2**63))
+        first = "random" if trial % 2 else "fixed"
+        pts = synth.random_cloud(n, int(rng.integers(0, 2**63)))
+        f = pcs.fps(pts, c, seed=seed, first=first)
+        a1 = pcs.afps(pts, c, 1, seed=seed, first=first)
+        assert f[0].tolist() == a1[0].tolist() and f[2] == a1[2]
+        nf = pcs.npdu_fps(pts, c, k, seed=seed, first=first)
+        na1 = pcs.npdu_afps(pts, c, 1, k, seed=seed, first=first)
+        assert nf[0].tolist() == na1[0].tolist() and nf[2] == na1[2]
+        big = pcs.npdu_fps(pts, c, 2 * n, seed=seed, first=first)
+        assert big[0].tolist() == f[0].tolist() and big[2] == f[2]
+        maxsec = -(-n // m)
+        wa = pcs.npdu_afps(pts, c, m, 2 * maxsec, seed=seed, first=first)
+        a = pcs.afps(pts, c, m, seed=seed, first=first)
+        assert wa[0].tolist() == a[0].tolist() and wa[2] == a[2]
+
+
+def test_random_configs_vs_oracle(pcs, oracle):
+    rng = np.random.default_rng(7777)
+    for t in range(160):
+        n = int(rng.integers(4, 3000 if t % 8 else 8193))
+        c = int(rng.integers(1, n + 1))
+        m = int(rng.integers(1, c + 1)) if t % 3 else 1
+        k = int(rng.integers(1, 200))
+        meth = ("fps", "afps", "npdu_fps", "npdu_afps")[t % 4]
+        first = "random" if t % 2 else "fixed"
+        pts = synth.random_cloud(n, 40000 + t)
+        if t % 5 == 0:
+            pts[: n // 2] = 1.0
+        if t % 7 == 0:
+            pts = np.round(pts)  # heavy ties
+        want = oracle.sample(meth, pts, c, m, k, first, t)
+        got = _call(pcs, meth, pts, c, m, k, first, t)
+        _same(got, *want)
+
+
+def test_distance_trace_bit_exact(pcs, oracle):
+    pts = synth.random_cloud(300, 404)
+    for k in (None, 7):
+        idx, _, st, tr = pcs.local_fps(pts, 40, 290, 60, k=k, seed=3, first="random", trace=True)
+        widx, wst, wtr = oracle.local_fps(pts, 40, 290, 60, k=k or 0, first="random", seed=3,
+                                          trace=True)
+        np.testing.assert_array_equal(idx, widx)
+        np.testing.assert_array_equal(tr, wtr)
+        assert (np.diff(tr, axis=0) <= 0).all()
+
+
+def test_batched_configs_vs_oracle(oracle):
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    cases = [
+        ("cfg1", synth.uniform_cube(1, 2048, 0), "fps", 512, 1, None, "x"),
+        ("cfg2", synth.primitives(16, 2048, 4, seed=1), "afps", 512, 8, None, "x"),
+        ("cfg3n", synth.primitives(4, 8192, 6, seed=3), "npdu_afps", 2048, 16, 65, "x"),
+        ("cfg3a", synth.primitives(2, 8192, 6, seed=3), "afps", 2048, 16, None, "x"),
+        ("cfg3f", synth.primitives(1, 8192, 6, seed=3), "fps", 2048, 1, None, "x"),
+        ("cfg4", synth.lidar_sweep(2, seed=4), "npdu_afps", 8192, 32, 129, None),
+        ("cfg5a", synth.uniform_cube(3, 4096, 9), "afps", 1024, 4, None, "x"),
+        ("cfg5n", synth.uniform_cube(3, 4096, 9), "npdu_afps", 1024, 16, 65, "x"),
+    ]
+    for name, xyz, meth, c, m, k, axis in cases:
+        dev = torch.from_numpy(xyz).cuda()
+        res = sample(dev, c, method=meth, m=m, k=k, sort=axis)
+        torch.cuda.synchronize()
+        if axis is not None:
+            host_sorted, order = synth.stable_sort_np(xyz, 0)
+            np.testing.assert_array_equal(res[-1].cpu().numpy(), order)
+            xyz = host_sorted
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k or 0)
+        np.testing.assert_array_equal(res[0].cpu().numpy(), want_idx, err_msg=name)
+        np.testing.assert_array_equal(res[1].cpu().numpy(), want_st.astype(np.int64), err_msg=name)
+
+
+def test_random_first_and_per_cloud_seeds(oracle):
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = synth.uniform_cube(6, 1000, 21)
+    seeds = torch.tensor([3, 99, 2**62 + 5, 0, 7, 123456789], dtype=torch.int64)
+    res = sample(torch.from_numpy(xyz).cuda(), 100, method="npdu_afps", m=5, k=17,
+                 first="random", seeds=seeds, index_dtype=torch.int64, return_sector=True)
+    for b in range(6):
+        idx, sec, st = oracle.sample("npdu_afps", xyz[b].astype(np.float64), 100, 5, 17,
+                                     "random", int(seeds[b]))
+        np.testing.assert_array_equal(res[0][b].cpu().numpy(), idx)
+        np.testing.assert_array_equal(res[2][b].cpu().numpy(), sec)
+        np.testing.assert_array_equal(res[1][b].cpu().numpy(), st.astype(np.int64))
+
+
+def test_sort_parity(pcs):
+    import torch
+
+    from paper_2208_08795_b200 import sort_axis
+
+    for name, g in load_sort_goldens().items():
+        np.testing.assert_array_equal(pcs.exact_sort(g["points"], "xyz"[int(name[-1])]), g["sorted"])
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 17, 1000, 16384, 16385, 40000):
+        xyz = np.round(rng.normal(size=(3, n, 3)), 2).astype(np.float32)
+        xyz[:, :: 7, 1] = -0.0
+        xyz[:, 1:: 7, 1] = 0.0
+        for axis in range(3):
+            out, perm = sort_axis(torch.from_numpy(xyz).cuda(), axis)
+            want, order = synth.stable_sort_np(xyz, axis)
+            np.testing.assert_array_equal(perm.cpu().numpy(), order)
+            np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_full_size_properties_cfg4():
+    """BASELINE cfg4 at full size (128 x 32768, NPDU-AFPS M=32, k=129,
+    C=8192): size-independent properties on every cloud, oracle on two."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = synth.lidar_sweep(128, seed=4)
+    idx, st, sec = sample(torch.from_numpy(xyz).cuda(), 8192, method="npdu_afps", m=32, k=129,
+                          return_sector=True)
+    idx, st, sec = idx.cpu().numpy(), st.cpu().numpy(), sec.cpu().numpy()
+    n, m, q = 32768, 32, 256
+    for b in range(128):
+        assert len(np.unique(idx[b])) == 8192
+        s = idx[b] // (n // m)
+        np.testing.assert_array_equal(s, sec[b])
+        np.testing.assert_array_equal(np.bincount(s, minlength=m), np.full(m, q))
+        # dist_evals == sum of the windows along the returned path
+        loc = (idx[b] % (n // m)).reshape(m, q)[:, :-1]
+        lo = np.maximum(loc - 64, 0)
+        hi = np.minimum(loc + 65, n // m)
+        assert st[b, 0] == (hi - lo).sum()
+        assert st[b, 2] == m * (q - 1) * (n // m) and st[b, 3] == m * (q - 1)
+        assert st[b, 1] <= st[b, 0]
+
+
+def test_determinism_across_calls():
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = torch.from_numpy(synth.primitives(8, 8192, 6, seed=5)).cuda()
+    a = sample(xyz, 2048, method="afps", m=16, sort="x")
+    b = sample(xyz, 2048, method="afps", m=16, sort="x")
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])

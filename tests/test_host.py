@@ -1,0 +1,165 @@
+"""CPU-only checks of the boundary and host logic: the C-ABI library loads and
+exports every entry point include/pcs_gpu.h declares, argument validation
+matches the reference's exceptions, the generators are deterministic, and the
+multi-GPU sharding math reproduces the single-process result (gloo, 2 ranks).
+No kernel is launched here."""
+import ctypes
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2208_08795_b200 import shard, synth
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "pcs_gpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pcs_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_cabi_exports_every_declared_symbol(pcs):
+    lib = ctypes.CDLL(pcs.LIB_PATH)
+    names = _declared_functions()
+    assert {"pcs_gpu_sample", "pcs_gpu_sort_axis", "pcs_sample_host", "pcs_local_fps_host",
+            "pcs_exact_sort_host", "pcs_last_error"} <= set(names)
+    for name in names:
+        assert hasattr(lib, name), name
+    lib.pcs_abi_version.restype = ctypes.c_int
+    assert lib.pcs_abi_version() == 1
+    lib.pcs_status_string.restype = ctypes.c_char_p
+    assert lib.pcs_status_string(1) == b"invalid argument"
+
+
+def test_cabi_rejects_before_touching_the_device(pcs):
+    # pcs_sample_host validates on the host first: no GPU needed for errors.
+    lib = ctypes.CDLL(pcs.LIB_PATH)
+    lib.pcs_last_error.restype = ctypes.c_char_p
+    pts = np.zeros((4, 3))
+    out = np.zeros(8, np.int64)
+    st = np.zeros(4, np.uint64)
+    rc = lib.pcs_sample_host(2, pts.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(4),
+                             ctypes.c_int64(3), ctypes.c_int64(5), ctypes.c_int64(0), 1,
+                             ctypes.c_uint64(0), 1, out.ctypes.data_as(ctypes.c_void_p),
+                             out.ctypes.data_as(ctypes.c_void_p), st.ctypes.data_as(ctypes.c_void_p))
+    assert rc == 1
+    assert lib.pcs_last_error() == b"partition_sectors: m exceeds point count"
+
+
+BAD = [("fps", 0, 1, 1), ("fps", 11, 1, 1), ("afps", 4, 5, 1), ("afps", 11, 2, 1),
+       ("afps", 4, 0, 1), ("npdu_afps", 4, 20, 3), ("npdu_fps", 4, 1, 0), ("npdu_afps", 4, 2, 0),
+       ("npdu_afps", 10, 10, 0)]
+
+
+@pytest.mark.parametrize("meth,c,m,k", BAD)
+def test_validation_messages_match_reference(pcs, reference, meth, c, m, k):
+    pts = synth.random_cloud(10, 1)
+    with pytest.raises(ValueError) as mine:
+        pcs._core.validate({"fps": 1, "afps": 2, "npdu_fps": 3, "npdu_afps": 4}[meth], 10, c, m, k)
+    with pytest.raises(ValueError) as ref:
+        reference.sample(meth, pts, c, m, k)
+    assert str(mine.value) == str(ref.value)
+
+
+def test_python_surface_matches_reference_signatures(pcs):
+    # proj/bindings/pcsample_module.cpp:150-190: names, kwargs, defaults
+    pts = synth.random_cloud(10, 1)
+    with pytest.raises(ValueError, match="c must be >= 1"):
+        pcs.fps(pts, 0)
+    with pytest.raises(ValueError, match="first must be 'random' or 'fixed'"):
+        pcs.afps(pts, 4, 2, seed=0, first="bogus", threads=4)
+    with pytest.raises(ValueError, match="expected an \\(N, 3\\) array"):
+        pcs.npdu_fps(np.zeros((4, 2)), 2, 3)
+    with pytest.raises(ValueError, match="axis must be x, y, or z"):
+        pcs.exact_sort(pts, axis="w")
+    with pytest.raises(ValueError, match="local_fps: window size must be >= 1"):
+        pcs.npdu_afps(pts, 4, 2, 0, seed=1, first="random", threads=2)
+
+
+def test_generators_deterministic_and_shaped():
+    a = synth.uniform_cube(2, 100, 5)
+    assert a.dtype == np.float32 and a.shape == (2, 100, 3)
+    np.testing.assert_array_equal(a, synth.uniform_cube(2, 100, 5))
+    assert np.abs(a).max() <= 1.0
+    p = synth.primitives(2, 2048, 4, seed=1)
+    assert p.shape == (2, 2048, 3) and np.isfinite(p).all()
+    assert np.linalg.norm(p, axis=-1).max() <= 1.0 + 1e-6
+    np.testing.assert_array_equal(p, synth.primitives(2, 2048, 4, seed=1))
+    lid = synth.lidar_sweep(1, seed=3)
+    r = np.linalg.norm(lid[0].astype(np.float64), axis=1)
+    assert lid.shape == (1, 32768, 3) and r.min() > 1.9 and r.max() < 80.2
+
+
+def test_split_and_sector_shards_tile_the_plan():
+    for total, world in [(128, 8), (10, 3), (3, 8), (1024, 8)]:
+        spans = [shard.split(total, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == total
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    n, c, m = 10007, 2501, 37
+    shards = [shard.sector_shard(n, c, m, 4, r) for r in range(4)]
+    assert shards[0].point_lo == 0 and shards[-1].point_hi == n
+    assert sum(s.c for s in shards) == c and sum(s.m for s in shards) == m
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, result_q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import Oracle
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    # one big cloud, AFPS sectors split across ranks (the 1M-point row of
+    # BASELINE cfg5 in miniature)
+    n, c, m, k = 4099, 1031, 16, 9
+    pts = synth.uniform_cube(1, n, 11)[0].astype(np.float64)
+    sh = shard.sector_shard(n, c, m, world, rank)
+    idx, sec, st = orc.sample("npdu_afps", pts[sh.point_lo:sh.point_hi], sh.c, sh.m, k)
+    local = torch.from_numpy(np.stack([idx + sh.point_lo, sec + sh.sector_lo], 1))
+    rows = shard.gather_rows(local, c, world)
+    stats = torch.from_numpy(st.astype(np.int64))
+    dist.all_reduce(stats)
+    # batch of clouds split by cloud
+    clouds = synth.uniform_cube(5, 300, 3)
+    b0, b1 = shard.split(5, world, rank)
+    bi, bst = orc.sample_batch_f32("afps", clouds[b0:b1], 64, 4) if b1 > b0 else (
+        np.zeros((0, 64), np.int64), np.zeros((0, 4), np.uint64))
+    brows = shard.gather_rows(torch.from_numpy(bi), 5, world)
+    if rank == 0:
+        result_q.put((rows.numpy(), stats.numpy(), brows.numpy()))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_sharding_equals_single_process(oracle):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    rows, stats, brows = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, c, m, k = 4099, 1031, 16, 9
+    pts = synth.uniform_cube(1, n, 11)[0].astype(np.float64)
+    idx, sec, st = oracle.sample("npdu_afps", pts, c, m, k)
+    np.testing.assert_array_equal(rows[:, 0], idx)
+    np.testing.assert_array_equal(rows[:, 1], sec)
+    np.testing.assert_array_equal(stats, st.astype(np.int64))
+    bi, _ = oracle.sample_batch_f32("afps", synth.uniform_cube(5, 300, 3), 64, 4)
+    np.testing.assert_array_equal(brows, bi)
