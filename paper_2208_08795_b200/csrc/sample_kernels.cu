@@ -209,22 +209,24 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
     const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
     unsigned long long best = 0;
     int bs = -1;
+    // Branch-free over the slots so independent slots interleave (ILP).
+    // Padding slots (j >= n) hold d = 0 and finite coordinates: they never
+    // win the argmax (best starts at 0 with a strict >) and their writes are
+    // masked out of the count.
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      if ((vmask >> k) & 1u) {
-        const int j = k * T + t;
-        const double xx = REGC ? x[REGC ? k : 0] : gs.xs[j];
-        const double yy = REGC ? y[REGC ? k : 0] : gs.ys[j];
-        const double zz = REGC ? z[REGC ? k : 0] : gs.zs[j];
-        const double dist = dist2(xx, yy, zz, px, py, pz);
-        const bool lower = dist <= d[k];
-        writes += lower ? 1u : 0u;
-        d[k] = lower ? dist : d[k];
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
-        if (bits > best) {
-          best = bits;
-          bs = k;
-        }
+      const int j = k * T + t;
+      const double xx = REGC ? x[REGC ? k : 0] : gs.xs[min(j, n - 1)];
+      const double yy = REGC ? y[REGC ? k : 0] : gs.ys[min(j, n - 1)];
+      const double zz = REGC ? z[REGC ? k : 0] : gs.zs[min(j, n - 1)];
+      const double dist = dist2(xx, yy, zz, px, py, pz);
+      const bool lower = dist <= d[k];
+      writes += (lower && ((vmask >> k) & 1u)) ? 1u : 0u;
+      d[k] = lower ? dist : d[k];
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+      if (bits > best) {
+        best = bits;
+        bs = k;
       }
     }
     if (p.trace) {
@@ -248,93 +250,146 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
 
 // ---------------------------------------------------------------- NPDU window
 // NPDU-FPS / NPDU-AFPS: the update touches only update_window(sector, idx, k)
-// (proj/src/sectors.cpp:53-61). The argmax still ranges over the whole
-// sector, but incrementally: lane s of each warp caches the max of that
-// warp's row s (points k*T + warp*32 + [0, 32)), and only rows the window
-// touched are re-reduced (3 redux each). Values only decrease, so untouched
-// rows keep valid maxima.
-template <int P, int W>
-__global__ void __launch_bounds__(W * 32 * (W >= 4 ? 1 : (4 / W)))
-    fps_window_kernel(const SampleParams p) {
-  static_assert(P <= 32, "row maxima are held one per lane");
+// (proj/src/sectors.cpp:53-61). One warp owns one sector; xyz (fp64) and the
+// min-distances d[] live in shared memory, so the rows of 32 points that a
+// window touches can be addressed with a runtime row index. The argmax still
+// ranges over the whole sector (as the reference's does), but
+// incrementally: each row's (max d, min index) is cached in registers --
+// lane l holds rows l, l+32, ... -- and only rows the window touched are
+// re-reduced (3 redux each). d only decreases, so untouched rows keep valid
+// maxima, and the per-iteration cost is O(k/32 + rows/32) instead of O(n).
+// Shared memory per NPDU warp: xyz + d (fp64) and the sampled bitmap,
+// rounded to 16 B so every warp's doubles stay aligned.
+__host__ __device__ __forceinline__ size_t npdu_warp_bytes(int nmax) {
+  return (size_t(32) * nmax + 4 * (nmax / 32 + 1) + 15) & ~size_t(15);
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(128) npdu_warp_kernel(const SampleParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int T = W * 32;
-  const int gid = threadIdx.x / T, t = threadIdx.x % T, lane = t & 31, warp = t >> 5;
+  const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long flat = static_cast<long long>(blockIdx.x) * p.G + gid;
+  if (flat >= p.B * p.M) return;
+  const long long b = flat / p.M, s = flat % p.M;
+  const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+  const int n = g.n, nmax = p.nmax;
+  unsigned char* base = smem + static_cast<size_t>(gid) * npdu_warp_bytes(nmax);
+  double* xs = reinterpret_cast<double*>(base);
+  double* ys = xs + nmax;
+  double* zs = ys + nmax;
+  double* d = zs + nmax;
+  unsigned* sampled = reinterpret_cast<unsigned*>(d + nmax);
+  const long long off = (b * p.N + g.begin) * 3;
+  if (p.f64)
+    stage_sector(static_cast<const double*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+  else
+    stage_sector(static_cast<const float*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = lane; j < n; j += 32) d[j] = kInf;
+  const int rows = (n + 31) >> 5;
+  for (int w = lane; w < rows; w += 32) sampled[w] = 0u;
+  if (p.out_sector)
+    for (int i = lane; i < g.quota; i += 32)
+      p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
+  // row maxima: lane l caches row r = l + 32*i in slot i; initially every
+  // point is +inf, so a row's winner is its first point
+  uint32_t rm_hi[RPL], rm_lo[RPL], rm_j[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    rm_hi[i] = r < rows ? kInfHi : 0u;
+    rm_lo[i] = 0u;
+    rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
+  }
   GroupSetup gs;
-  if (!setup_group<W>(p, smem, gid, t, gs)) return;
-  const int n = gs.g.n;
+  gs.b = b;
+  gs.s = s;
+  gs.g = g;
+  int cur = first_point(p, gs);
+  if (lane == 0) {
+    write_index(p, b, g.out_off, g.begin + cur);
+    sampled[cur >> 5] |= 1u << (cur & 31);
+  }
+  __syncwarp();
   const long long K = p.K;
   const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
-  group_sync<W>(gid);
-
-  double d[P];
-  unsigned vmask = 0;
-  uint32_t rm_hi = 0, rm_lo = 0, rm_j = kNoIndex;
-#pragma unroll
-  for (int k = 0; k < P; ++k) {
-    const int j = k * T + t;
-    const bool valid = j < n;
-    vmask |= valid ? (1u << k) : 0u;
-    d[k] = valid ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
-    uint32_t hi = valid ? kInfHi : 0u, lo = 0, jj = valid ? static_cast<uint32_t>(j) : kNoIndex;
-    warp_argmax(hi, lo, jj);
-    if (lane == k) {
-      rm_hi = hi;
-      rm_lo = lo;
-      rm_j = jj;
-    }
-  }
-
-  int cur = first_point(p, gs);
-  if (t == 0) write_index(p, gs.b, gs.g.out_off, gs.g.begin + cur);
-  unsigned smask = (cur % T == t) ? (1u << (cur / T)) : 0u;
   unsigned writes = 0;
   unsigned long long evals = 0;
-  int round = 0;
 
-  for (int it = 1; it < gs.g.quota; ++it) {
-    const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
+  for (int it = 1; it < g.quota; ++it) {
+    const double px = xs[cur], py = ys[cur], pz = zs[cur];
     const int wb = cur >= half_down ? cur - half_down : 0;
     const int we = min(n, cur + half_up);
     evals += static_cast<unsigned long long>(we - wb);
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int r0 = k * T + warp * 32;
-      if (r0 < we && r0 + 32 > wb) {  // warp-uniform: row k of this warp is touched
-        const int j = r0 + lane;
-        if (j >= wb && j < we) {
-          const double dist = dist2(gs.xs[j], gs.ys[j], gs.zs[j], px, py, pz);
-          const bool lower = dist <= d[k];
-          writes += lower ? 1u : 0u;
-          d[k] = lower ? dist : d[k];
-        }
-        const bool valid = (vmask >> k) & 1u;
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
-        uint32_t hi = valid ? static_cast<uint32_t>(bits >> 32) : 0u;
-        uint32_t lo = valid ? static_cast<uint32_t>(bits) : 0u;
-        uint32_t jj = valid ? static_cast<uint32_t>(j) : kNoIndex;
-        warp_argmax(hi, lo, jj);
-        if (lane == k) {
-          rm_hi = hi;
-          rm_lo = lo;
-          rm_j = jj;
+    const int r_lo = wb >> 5, r_hi = (we - 1) >> 5;
+#pragma unroll 2
+    for (int r = r_lo; r <= r_hi; ++r) {
+      const int j = (r << 5) + lane;
+      double dj = j < n ? d[j] : 0.0;
+      if (j >= wb && j < we) {
+        const double dist = dist2(xs[j], ys[j], zs[j], px, py, pz);
+        const bool lower = dist <= dj;
+        writes += lower ? 1u : 0u;
+        if (lower) {
+          dj = dist;
+          d[j] = dist;
         }
       }
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(dj));
+      uint32_t hi = static_cast<uint32_t>(bits >> 32), lo = static_cast<uint32_t>(bits);
+      uint32_t jj = j < n ? static_cast<uint32_t>(j) : kNoIndex;
+      warp_argmax(hi, lo, jj);
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if ((r >> 5) == i && (r & 31) == lane) {
+          rm_hi[i] = hi;
+          rm_lo[i] = lo;
+          rm_j[i] = jj;
+        }
     }
     if (p.trace) {
-#pragma unroll
-      for (int k = 0; k < P; ++k)
-        if ((vmask >> k) & 1u) p.trace[static_cast<long long>(it - 1) * n + k * T + t] = d[k];
+      __syncwarp();
+      for (int j = lane; j < n; j += 32) p.trace[static_cast<long long>(it - 1) * n + j] = d[j];
     }
-    uint32_t hi = rm_hi, lo = rm_lo, j = rm_j;
-    group_argmax<W>(hi, lo, j, gs.cand, round, gid, lane, warp);
-    if ((hi | lo) == 0u)
-      j = lowest_unsampled<P, W>(vmask, smask, t, gs.cand, round, gid, lane, warp);
+    // whole-sector argmax from the cached row maxima; rows l + 32*i grow with
+    // i, so a strict > keeps the lowest index among equal distances
+    uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
+#pragma unroll
+    for (int i = 1; i < RPL; ++i) {
+      const bool gt = rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo);
+      hi = gt ? rm_hi[i] : hi;
+      lo = gt ? rm_lo[i] : lo;
+      j = gt ? rm_j[i] : j;
+    }
+    warp_argmax(hi, lo, j);
+    if ((hi | lo) == 0u) {
+      // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
+      uint32_t jm = kNoIndex;
+      for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+        const unsigned free_bits = ~sampled[w];
+        if (free_bits) {
+          const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
+          if (cand < static_cast<uint32_t>(n)) jm = cand;
+        }
+      }
+      j = __reduce_min_sync(kFull, jm);
+    }
     cur = static_cast<int>(j);
-    if (t == 0) write_index(p, gs.b, gs.g.out_off + it, gs.g.begin + cur);
-    if (cur % T == t) smask |= 1u << (cur / T);
+    if (lane == 0) {
+      write_index(p, b, g.out_off + it, g.begin + cur);
+      sampled[cur >> 5] |= 1u << (cur & 31);
+    }
+    __syncwarp();
   }
-  flush_stats<W>(p, gs, t, writes, evals);
+  const unsigned ws = __reduce_add_sync(kFull, writes);
+  if (p.stats && lane == 0) {
+    unsigned long long* st = p.stats + b * 4;
+    const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
+    if (ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
+    atomicAdd(st + 0, evals);
+    atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
+    atomicAdd(st + 3, iters);
+  }
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -373,10 +428,22 @@ cudaError_t run_full(SampleParams p, cudaStream_t st) {
   return launch_groups(fps_full_kernel<P, W, REGC>, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
 }
 
-template <int P, int W>
-cudaError_t run_window(SampleParams p, cudaStream_t st) {
-  const int G = pick_groups(p.B * p.M, W, p.nmax, W >= 4 ? W * 32 : 128);
-  return launch_groups(fps_window_kernel<P, W>, p, W, std::min(G, W >= 4 ? 1 : 4 / W), st);
+template <int RPL>
+cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
+  const size_t warp_bytes = npdu_warp_bytes(p.nmax);
+  int G = 4;
+  while (G > 1 && warp_bytes * G > 110 * 1024) G /= 2;
+  while (G > 1 && (p.B * p.M + G - 1) / G < 2 * 148) G /= 2;
+  const size_t smem = warp_bytes * G;
+  if (smem > kMaxSmem) return cudaErrorNotSupported;
+  auto kern = npdu_warp_kernel<RPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  p.G = G;
+  const long long blocks = (p.B * p.M + G - 1) / G;
+  kern<<<static_cast<unsigned>(blocks), 32 * G, smem, st>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
@@ -394,15 +461,12 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
     if (n <= 4096) return run_full<16, 8, true>(p, st);
     if (n <= 8192) return run_full<8, 32, false>(p, st);
   } else {
-    if (n <= 32) return run_window<1, 1>(p, st);
-    if (n <= 64) return run_window<2, 1>(p, st);
-    if (n <= 128) return run_window<4, 1>(p, st);
-    if (n <= 256) return run_window<8, 1>(p, st);
-    if (n <= 512) return run_window<16, 1>(p, st);
-    if (n <= 1024) return run_window<32, 1>(p, st);
-    if (n <= 2048) return run_window<32, 2>(p, st);
-    if (n <= 4096) return run_window<32, 4>(p, st);
-    if (n <= 8192) return run_window<32, 8>(p, st);
+    cudaError_t e = cudaErrorNotSupported;
+    if (n <= 1024) e = run_npdu<1>(p, st);
+    else if (n <= 2048) e = run_npdu<2>(p, st);
+    else if (n <= 4096) e = run_npdu<4>(p, st);
+    else if (n <= 7040) e = run_npdu<8>(p, st);
+    if (e != cudaErrorNotSupported) return e;
   }
   if (msg) *msg = "sector of " + std::to_string(n) + " points exceeds the on-chip sampler (8192)";
   return cudaErrorNotSupported;
