@@ -1,0 +1,129 @@
+// Full-window FPS / AFPS kernels (see sampler_common.cuh for the layout).
+#include "sampler_common.cuh"
+
+namespace pcsk {
+
+// ---------------------------------------------------------------- full window
+// FPS / AFPS: every iteration updates the whole sector (sampler.cpp:115-129
+// with window == sector). REGC: sector xyz also cached in registers.
+template <int P, int W, bool REGC>
+__global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
+    fps_full_kernel(const SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int T = W * 32;
+  const int gid = threadIdx.x / T, t = threadIdx.x % T, lane = t & 31, warp = t >> 5;
+  GroupSetup gs;
+  if (!setup_group<W>(p, smem, gid, t, gs)) return;
+  const int n = gs.g.n;
+  group_sync<W>(gid);
+
+  double x[REGC ? P : 1], y[REGC ? P : 1], z[REGC ? P : 1], d[P];
+  unsigned vmask = 0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int j = k * T + t;
+    const bool valid = j < n;
+    vmask |= valid ? (1u << k) : 0u;
+    if constexpr (REGC) {
+      x[k] = valid ? gs.xs[j] : 0.0;
+      y[k] = valid ? gs.ys[j] : 0.0;
+      z[k] = valid ? gs.zs[j] : 0.0;
+    }
+    d[k] = valid ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+  }
+
+  int cur = first_point(p, gs);
+  if (t == 0) write_index(p, gs.b, gs.g.out_off, gs.g.begin + cur);
+  unsigned smask = (cur % T == t) ? (1u << (cur / T)) : 0u;
+  unsigned writes = 0;
+  int round = 0;
+
+  for (int it = 1; it < gs.g.quota; ++it) {
+    const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
+    unsigned long long best = 0;
+    int bs = -1;
+    // Branch-free over the slots so independent slots interleave (ILP).
+    // Padding slots (j >= n) hold d = 0 and finite coordinates: they never
+    // win the argmax (best starts at 0 with a strict >) and their writes are
+    // masked out of the count.
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int j = k * T + t;
+      const double xx = REGC ? x[REGC ? k : 0] : gs.xs[min(j, n - 1)];
+      const double yy = REGC ? y[REGC ? k : 0] : gs.ys[min(j, n - 1)];
+      const double zz = REGC ? z[REGC ? k : 0] : gs.zs[min(j, n - 1)];
+      const double dist = dist2(xx, yy, zz, px, py, pz);
+      const bool lower = dist <= d[k];
+      writes += (lower && ((vmask >> k) & 1u)) ? 1u : 0u;
+      d[k] = lower ? dist : d[k];
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+      if (bits > best) {
+        best = bits;
+        bs = k;
+      }
+    }
+    if (p.trace) {
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        if ((vmask >> k) & 1u) p.trace[static_cast<long long>(it - 1) * n + k * T + t] = d[k];
+    }
+    uint32_t hi = static_cast<uint32_t>(best >> 32), lo = static_cast<uint32_t>(best);
+    uint32_t j = bs >= 0 ? static_cast<uint32_t>(bs * T + t) : kNoIndex;
+    group_argmax<W>(hi, lo, j, gs.cand, round, gid, lane, warp);
+    if ((hi | lo) == 0u)
+      j = lowest_unsampled<P, W>(vmask, smask, t, gs.cand, round, gid, lane, warp);
+    cur = static_cast<int>(j);
+    if (t == 0) write_index(p, gs.b, gs.g.out_off + it, gs.g.begin + cur);
+    if (cur % T == t) smask |= 1u << (cur / T);
+  }
+  const unsigned long long evals =
+      static_cast<unsigned long long>(gs.g.quota - 1) * static_cast<unsigned long long>(n);
+  flush_stats<W>(p, gs, t, writes, evals);
+}
+
+template <typename Kern>
+cudaError_t launch_groups(Kern kern, SampleParams p, int W, int G, cudaStream_t st) {
+  const size_t group_bytes = size_t(24) * p.nmax + 32 * W;
+  const size_t smem = group_bytes * G;
+  if (smem > kMaxSmem) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  p.G = G;
+  const long long sectors = p.B * p.M;
+  const long long blocks = (sectors + G - 1) / G;
+  kern<<<static_cast<unsigned>(blocks), G * W * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+// Groups per CTA: up to `max_threads` threads and ~110 KB of shared memory
+// (two CTAs per SM), fewer when there are not enough sectors to fill the SMs.
+int pick_groups(long long sectors, int W, int nmax, int max_threads) {
+  const size_t group_bytes = size_t(24) * nmax + 32 * W;
+  int G = std::max(1, max_threads / (W * 32));
+  if (W > 1) G = std::min(G, 15);  // named barriers 1..15
+  while (G > 1 && group_bytes * G > 110 * 1024) G /= 2;
+  while (G > 1 && (sectors + G - 1) / G < 2 * 148) G /= 2;
+  return G;
+}
+
+template <int P, int W, bool REGC>
+cudaError_t run_full(SampleParams p, cudaStream_t st) {
+  const int G = pick_groups(p.B * p.M, W, p.nmax, W >= 8 ? W * 32 : 256);
+  return launch_groups(fps_full_kernel<P, W, REGC>, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
+}
+
+cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
+  if (n <= 32) return run_full<1, 1, true>(p, st);
+  if (n <= 64) return run_full<2, 1, true>(p, st);
+  if (n <= 128) return run_full<4, 1, true>(p, st);
+  if (n <= 256) return run_full<8, 1, true>(p, st);
+  if (n <= 512) return run_full<16, 1, true>(p, st);
+  if (n <= 1024) return run_full<16, 2, true>(p, st);
+  if (n <= 2048) return run_full<16, 4, true>(p, st);
+  if (n <= 4096) return run_full<16, 8, true>(p, st);
+  if (n <= 8192) return run_full<8, 32, false>(p, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace pcsk

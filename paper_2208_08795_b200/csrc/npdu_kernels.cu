@@ -1,0 +1,286 @@
+// NPDU-FPS / NPDU-AFPS kernels for sm_100a.
+//
+// The update touches only update_window(sector, idx, k) (proj/src/
+// sectors.cpp:53-61): the k storage neighbours of the pivot. One warp owns
+// one sector. xyz and the fp64 min-distances d[] live in shared memory, so
+// the rows of 32 points a window touches are addressed with a runtime row
+// index; fp32 inputs stay fp32 there (widened exactly on use), which halves
+// the footprint and doubles the sectors resident per SM.
+//
+// The argmax still ranges over the whole sector, as the reference's does
+// (sampler.cpp:137-154), but incrementally: each row's (max d, min index) is
+// cached in registers -- lane l holds rows l, l+32, ... -- and only rows the
+// window touched are re-reduced. d only decreases, so untouched rows keep
+// valid maxima; an iteration costs O(k/32 + rows/32) instead of O(n).
+//
+// Shared arrays are padded with whole rows past the sector end (d = 0,
+// xyz = 0): the window's rows are processed branch-free and unclamped, pad
+// lanes never write (the window ends inside the sector) and never win the
+// argmax (their d = 0 can only tie a max of 0, which takes the lowest-
+// unsampled path).
+#include "sampler_common.cuh"
+
+namespace pcsk {
+
+// Rows of padding after the sector: the RMAX-unrolled path reads up to
+// RMAX-1 rows past the window's last row; the runtime loop reads one.
+__host__ __device__ constexpr int npdu_pad_rows(int rmax) { return rmax > 2 ? rmax : 2; }
+
+__host__ __device__ __forceinline__ int npdu_padded(int nmax, int rmax) {
+  return (((nmax + 31) >> 5) + npdu_pad_rows(rmax)) << 5;
+}
+
+template <typename CT>
+__host__ __device__ __forceinline__ size_t npdu_warp_bytes(int nmax, int rmax) {
+  const size_t np = static_cast<size_t>(npdu_padded(nmax, rmax));
+  return (np * (8 + 3 * sizeof(CT)) + np / 8 + 15) & ~size_t(15);
+}
+
+// (max d, min index) of row r. Within a row the index grows with the lane,
+// so the lowest lane holding the max is the winner: two reductions and a
+// ballot instead of three reductions.
+__device__ __forceinline__ void row_key(double dj, int r, uint32_t& hi, uint32_t& lo,
+                                        uint32_t& j) {
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(dj));
+  const uint32_t h = static_cast<uint32_t>(bits >> 32), l = static_cast<uint32_t>(bits);
+  const uint32_t mh = __reduce_max_sync(kFull, h);
+  const uint32_t ml = __reduce_max_sync(kFull, h == mh ? l : 0u);
+  const unsigned cand = __ballot_sync(kFull, h == mh && l == ml);
+  hi = mh;
+  lo = ml;
+  j = static_cast<uint32_t>((r << 5) + __ffs(cand) - 1);
+}
+
+template <int RPL>
+__device__ __forceinline__ void store_row(int r, int lane, uint32_t hi, uint32_t lo, uint32_t j,
+                                          uint32_t (&rh)[RPL], uint32_t (&rl)[RPL],
+                                          uint32_t (&rj)[RPL]) {
+#pragma unroll
+  for (int i = 0; i < RPL; ++i)
+    if (r == lane + 32 * i) {
+      rh[i] = hi;
+      rl[i] = lo;
+      rj[i] = j;
+    }
+}
+
+// RMAX > 0: a window spans at most RMAX rows (ceil((k+31)/32)); all RMAX are
+// processed unconditionally and unrolled in phases (all loads, then the fp64
+// chains, then the stores, then the reductions) so the rows overlap. Rows
+// past the window get no writes and re-reduce to their cached value.
+// RMAX == 0: runtime row loop (wide windows).
+template <typename CT, int RPL, int RMAX>
+__global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long flat = static_cast<long long>(blockIdx.x) * p.G + gid;
+  if (flat >= p.B * p.M) return;
+  const long long b = flat / p.M, s = flat % p.M;
+  const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+  const int n = g.n, np = npdu_padded(p.nmax, RMAX);
+  unsigned char* base = smem + static_cast<size_t>(gid) * npdu_warp_bytes<CT>(p.nmax, RMAX);
+  double* d = reinterpret_cast<double*>(base);
+  CT* xs = reinterpret_cast<CT*>(d + np);
+  CT* ys = xs + np;
+  CT* zs = ys + np;
+  unsigned* sampled = reinterpret_cast<unsigned*>(zs + np);
+  if (sizeof(CT) < sizeof(double) && p.f64) __trap();  // fp32 staging is fp32-input only
+  {
+    const long long off = (b * p.N + g.begin) * 3;
+    if (p.f64)
+      stage_sector(static_cast<const double*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+    else
+      stage_sector(static_cast<const float*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+  }
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = lane; j < np; j += 32) {
+    d[j] = j < n ? kInf : 0.0;
+    if (j >= n) xs[j] = ys[j] = zs[j] = CT(0);
+  }
+  const int rows = (n + 31) >> 5;
+  for (int w = lane; w < (np >> 5); w += 32) sampled[w] = 0u;
+  if (p.out_sector)
+    for (int i = lane; i < g.quota; i += 32)
+      p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
+  // row maxima: lane l caches row r = l + 32*i in slot i; initially every
+  // point is +inf, so a row's winner is its first point
+  uint32_t rm_hi[RPL], rm_lo[RPL], rm_j[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    rm_hi[i] = r < rows ? kInfHi : 0u;
+    rm_lo[i] = 0u;
+    rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
+  }
+  GroupSetup gs;
+  gs.b = b;
+  gs.s = s;
+  gs.g = g;
+  int cur = first_point(p, gs);
+  // output row of this sector; index written = begin + index_base + local
+  const long long out_base = b * p.C + g.out_off;
+  const long long index_off = g.begin + p.index_base;
+  int* out32 = static_cast<int*>(p.out_idx) + out_base;
+  long long* out64 = static_cast<long long*>(p.out_idx) + out_base;
+  if (lane == 0) {
+    if (p.idx64) out64[0] = index_off + cur;
+    else out32[0] = static_cast<int>(index_off + cur);
+    sampled[cur >> 5] |= 1u << (cur & 31);
+  }
+  __syncwarp();
+  const long long K = p.K;
+  const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
+  unsigned writes = 0;
+  unsigned long long evals = 0;
+  double* const trace = p.trace;
+
+  for (int it = 1; it < g.quota; ++it) {
+    const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
+                 pz = static_cast<double>(zs[cur]);
+    const int wb = cur >= half_down ? cur - half_down : 0;
+    const int we = min(n, cur + half_up);
+    evals += static_cast<unsigned long long>(we - wb);
+    const int r_lo = wb >> 5;
+    if constexpr (RMAX > 0) {
+      const int j0 = (r_lo << 5) + lane;
+      double dj[RMAX], dist[RMAX];
+      bool lower[RMAX];
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int j = j0 + 32 * q;
+        dj[q] = d[j];
+        dist[q] = dist2(static_cast<double>(xs[j]), static_cast<double>(ys[j]),
+                        static_cast<double>(zs[j]), px, py, pz);
+      }
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int j = j0 + 32 * q;
+        lower[q] = j >= wb && j < we && dist[q] <= dj[q];
+        writes += lower[q] ? 1u : 0u;
+        dj[q] = lower[q] ? dist[q] : dj[q];
+      }
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q)
+        if (lower[q]) d[j0 + 32 * q] = dist[q];
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        uint32_t hi, lo, jj;
+        row_key(dj[q], r_lo + q, hi, lo, jj);
+        store_row<RPL>(r_lo + q, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+      }
+    } else {
+      const int r_hi = (we - 1) >> 5;
+      for (int r = r_lo; r <= r_hi; r += 2) {
+        const int ja = (r << 5) + lane, jb = ja + 32;
+        double da = d[ja], db = d[jb];
+        const double ea = dist2(static_cast<double>(xs[ja]), static_cast<double>(ys[ja]),
+                                static_cast<double>(zs[ja]), px, py, pz);
+        const double eb = dist2(static_cast<double>(xs[jb]), static_cast<double>(ys[jb]),
+                                static_cast<double>(zs[jb]), px, py, pz);
+        const bool la = ja >= wb && ja < we && ea <= da;
+        const bool lb = jb >= wb && jb < we && eb <= db;
+        writes += (la ? 1u : 0u) + (lb ? 1u : 0u);
+        if (la) d[ja] = ea;
+        if (lb) d[jb] = eb;
+        da = la ? ea : da;
+        db = lb ? eb : db;
+        uint32_t hi, lo, jj;
+        row_key(da, r, hi, lo, jj);
+        store_row<RPL>(r, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+        row_key(db, r + 1, hi, lo, jj);
+        store_row<RPL>(r + 1, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+      }
+    }
+    if (trace) {
+      __syncwarp();
+      for (int j = lane; j < n; j += 32) trace[static_cast<long long>(it - 1) * n + j] = d[j];
+    }
+    // whole-sector argmax from the cached row maxima; rows l + 32*i grow with
+    // i, so a strict > keeps the lowest index among equal distances
+    uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
+#pragma unroll
+    for (int i = 1; i < RPL; ++i) {
+      const bool gt = rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo);
+      hi = gt ? rm_hi[i] : hi;
+      lo = gt ? rm_lo[i] : lo;
+      j = gt ? rm_j[i] : j;
+    }
+    warp_argmax(hi, lo, j);
+    if ((hi | lo) == 0u) {
+      // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
+      uint32_t jm = kNoIndex;
+      for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+        const unsigned free_bits = ~sampled[w];
+        if (free_bits) {
+          const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
+          if (cand < static_cast<uint32_t>(n)) jm = cand;
+        }
+      }
+      j = __reduce_min_sync(kFull, jm);
+    }
+    cur = static_cast<int>(j);
+    if (lane == 0) {
+      if (p.idx64) out64[it] = index_off + cur;
+      else out32[it] = static_cast<int>(index_off + cur);
+      sampled[cur >> 5] |= 1u << (cur & 31);
+    }
+    __syncwarp();
+  }
+  const unsigned ws = __reduce_add_sync(kFull, writes);
+  if (p.stats && lane == 0) {
+    unsigned long long* st = p.stats + b * 4;
+    const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
+    if (ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
+    atomicAdd(st + 0, evals);
+    atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
+    atomicAdd(st + 3, iters);
+  }
+}
+
+template <typename CT, int RPL, int RMAX>
+cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
+  const size_t warp_bytes = npdu_warp_bytes<CT>(p.nmax, RMAX);
+  // warps per CTA: as many as shared memory lets one SM hold (one CTA per SM
+  // when the batch is large), but never so many that CTAs < SMs
+  const long long per_sm = static_cast<long long>(kMaxSmem / warp_bytes);
+  const long long sectors = p.B * p.M;
+  const int G = static_cast<int>(std::max(1LL, std::min({16LL, per_sm, sectors / 148})));
+  const size_t smem = warp_bytes * G;
+  if (smem > kMaxSmem) return cudaErrorNotSupported;
+  auto kern = npdu_warp_kernel<CT, RPL, RMAX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  p.G = G;
+  const long long blocks = (sectors + G - 1) / G;
+  kern<<<static_cast<unsigned>(blocks), 32 * G, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename CT, int RPL>
+cudaError_t run_npdu_rows(SampleParams p, cudaStream_t st) {
+  const long long rows_needed = (p.K + 31) / 32;  // rows one window can touch
+  if (rows_needed <= 2) return run_npdu<CT, RPL, 2>(p, st);
+  if (rows_needed <= 3) return run_npdu<CT, RPL, 3>(p, st);
+  if (rows_needed <= 5) return run_npdu<CT, RPL, 5>(p, st);
+  return run_npdu<CT, RPL, 0>(p, st);
+}
+
+template <int RPL>
+cudaError_t run_npdu_rpl(SampleParams p, cudaStream_t st) {
+  if (p.f64) return run_npdu_rows<double, RPL>(p, st);
+  // fp32 input: stage fp32 (widened exactly on use) unless fp64 staging
+  // still fits 16 warps per SM
+  if (npdu_warp_bytes<double>(p.nmax, 5) * 16 <= kMaxSmem) return run_npdu_rows<double, RPL>(p, st);
+  return run_npdu_rows<float, RPL>(p, st);
+}
+
+cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
+  if (n <= 1024) return run_npdu_rpl<1>(p, st);
+  if (n <= 2048) return run_npdu_rpl<2>(p, st);
+  if (n <= 4096) return run_npdu_rpl<4>(p, st);
+  if (n <= 8192) return run_npdu_rpl<8>(p, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace pcsk

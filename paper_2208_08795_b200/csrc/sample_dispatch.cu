@@ -1,0 +1,79 @@
+// Batched sampler entry: picks the kernel family per sector size and window.
+#include "sampler_common.cuh"
+
+namespace pcsk {
+
+cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
+                     std::string* msg) {
+  p.nmax = static_cast<int>((nmax_sector + 1) & ~1LL);
+  const cudaError_t e = windowed ? run_npdu_any(p, nmax_sector, st)
+                                 : run_full_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && msg)
+    *msg = "sector of " + std::to_string(nmax_sector) +
+           " points exceeds the on-chip samplers of this build";
+  return e;
+}
+
+}  // namespace pcsk
+
+namespace pcs_internal {
+
+cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::string* msg) {
+  const bool sectored = a.method == PCS_METHOD_AFPS || a.method == PCS_METHOD_NPDU_AFPS;
+  const bool windowed = a.method == PCS_METHOD_NPDU_FPS || a.method == PCS_METHOD_NPDU_AFPS;
+  const long long M = sectored ? a.m : 1;
+  const long long nmax = (a.n + M - 1) / M;
+  pcsk::SampleParams p{};
+  p.xyz = a.xyz;
+  p.f64 = a.coord_dtype == PCS_DTYPE_F64;
+  p.B = a.batch;
+  p.N = a.n;
+  p.C = a.c;
+  p.M = M;
+  // A window that always covers the whole sector is the full update
+  // (k >= 2*n-1 => update_window == sector for every pivot), and the
+  // OpStats agree: every window then holds the sector's n points.
+  p.K = (windowed && a.k < 2 * nmax - 1) ? a.k : 0;
+  p.random_first = a.seed_policy == PCS_RANDOM_FIRST_POINT;
+  p.seed = a.seed;
+  p.seeds = a.seeds;
+  p.out_idx = a.out_indices;
+  p.idx64 = a.index_dtype == PCS_INDEX_I64;
+  p.out_sector = a.out_sector;
+  p.stats = reinterpret_cast<unsigned long long*>(a.out_stats);
+  p.index_base = a.index_base;
+  p.sector_base = a.sector_base;
+  if (a.out_stats) {
+    cudaError_t e = cudaMemsetAsync(a.out_stats, 0, sizeof(uint64_t) * 4 * a.batch, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+}
+
+cudaError_t launch_local_fps(const double* xyz, int64_t n, int64_t sb, int64_t se,
+                             int64_t quota, int64_t k, int random_first, uint64_t seed,
+                             int64_t* out_idx, uint64_t* out_stats, double* trace,
+                             cudaStream_t stream, std::string* msg) {
+  (void)n;
+  const long long len = se - sb;
+  pcsk::SampleParams p{};
+  p.xyz = xyz + 3 * sb;
+  p.f64 = 1;
+  p.B = 1;
+  p.N = len;
+  p.C = quota;
+  p.M = 1;
+  p.K = (k > 0 && k < 2 * len - 1) ? k : 0;
+  p.random_first = random_first;
+  p.seed = seed;
+  p.out_idx = out_idx;
+  p.idx64 = 1;
+  p.index_base = sb;
+  p.stats = reinterpret_cast<unsigned long long*>(out_stats);
+  p.trace = trace;
+  cudaError_t e = cudaMemsetAsync(out_stats, 0, sizeof(uint64_t) * 4, stream);
+  if (e != cudaSuccess) return e;
+  return pcsk::dispatch(p, len, p.K > 0, stream, msg);
+}
+
+}  // namespace pcs_internal
