@@ -52,6 +52,11 @@ for _n in (2048, 4096, 8192, 16384, 32768):
     WORKLOADS[f"cfg5-npdu-{_n}"] = dict(gen="cube", B=256, N=_n, method="npdu_afps", C=_n // 4,
                                         M=16, K=65, sort="x")
 
+# latency probes: one NPDU sector per warp, 1 warp / 148 warps / 4096 warps
+for _b in (1, 148, 4096):
+    WORKLOADS[f"lat-npdu-{_b}"] = dict(gen="cube", B=_b, N=1024, method="npdu_fps", C=256, M=1,
+                                       K=129, sort=None)
+
 DEFAULT_WORKLOAD = "cfg4"
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
 

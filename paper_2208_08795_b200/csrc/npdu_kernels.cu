@@ -259,7 +259,8 @@ cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
 
 template <typename CT, int RPL>
 cudaError_t run_npdu_rows(SampleParams p, cudaStream_t st) {
-  const long long rows_needed = (p.K + 31) / 32;  // rows one window can touch
+  // rows a window of K consecutive points can touch: ceil((K + 31) / 32)
+  const long long rows_needed = (p.K + 62) / 32;
   if (rows_needed <= 2) return run_npdu<CT, RPL, 2>(p, st);
   if (rows_needed <= 3) return run_npdu<CT, RPL, 3>(p, st);
   if (rows_needed <= 5) return run_npdu<CT, RPL, 5>(p, st);

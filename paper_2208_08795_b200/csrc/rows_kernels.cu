@@ -1,0 +1,445 @@
+// Pruned-row sampler for large sectors (FPS / AFPS / NPDU variants), sm_100a.
+//
+// A sector (up to the whole cloud) lives on chip in one CTA, or split into
+// row-aligned chunks over a thread-block cluster of CS CTAs: xyz (input type)
+// and the fp64 min-distances d[] in shared memory. Points are grouped in rows
+// of 32 consecutive storage indices. Every row keeps, in the registers of the
+// lane that owns it, (a) its exact argmax key (max d bits, min index) and a
+// float upper bound of that max, and (b) a float bounding box of its points.
+//
+// One iteration of local_fps (proj/src/sampler.cpp:114-161):
+//   1. every lane tests its rows: a row can only change if some point of it
+//      can get closer to the pivot than the row's current max d. The test is
+//      a rigorous lower bound -- box-to-pivot squared distance in fp32 with
+//      round-down arithmetic, shrunk by 2^-20 to cover the fp64 evaluation's
+//      own rounding (< 5 * 2^-53 relative) -- against the row max rounded up.
+//      A skipped row provably has dist > d[j] for every j: no write, no
+//      change of its maximum. The decision never changes a result or a
+//      counter; it only avoids work. (NPDU additionally restricts the rows to
+//      the update window, proj/src/sectors.cpp:53-61.)
+//   2. the surviving rows are updated exactly (fp64, reference operation
+//      order, `dist <= d` rule) and re-reduced (2 redux + ballot);
+//   3. warp -> CTA (shared memory, one barrier) -> cluster (DSMEM stores, one
+//      cluster barrier) argmax on (max d, min index); candidates carry their
+//      coordinates so the next pivot needs no lookup.
+// dist_evals / argmax_scans / iterations are the reference's counts (the
+// whole window is "evaluated" in its accounting: sampler.cpp:129, 155);
+// dist_writes counts actual writes, which skipped rows provably have none of.
+#include <cooperative_groups.h>
+
+#include "sampler_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pcsk {
+
+namespace {
+
+constexpr int kRowsPad = 2;  // zero rows after each chunk (pair processing)
+
+struct Cand {
+  uint32_t hi, lo, j, pad;
+  double x, y, z;
+};
+
+__device__ __forceinline__ float f_lo(float v) { return v; }
+__device__ __forceinline__ float f_hi(float v) { return v; }
+__device__ __forceinline__ float f_lo(double v) { return __double2float_rd(v); }
+__device__ __forceinline__ float f_hi(double v) { return __double2float_ru(v); }
+
+// Lower bound (round-down fp32) of the squared distance from the pivot
+// interval [pl, ph] to the box [b0, b1] on one axis.
+__device__ __forceinline__ float gap2(float b0, float b1, float pl, float ph) {
+  const float g = fmaxf(fmaxf(__fsub_rd(b0, ph), __fsub_rd(pl, b1)), 0.0f);
+  return __fmul_rd(g, g);
+}
+
+__device__ __forceinline__ bool key_gt(uint32_t h1, uint32_t l1, uint32_t j1, uint32_t h2,
+                                       uint32_t l2, uint32_t j2) {
+  return h1 > h2 || (h1 == h2 && (l1 > l2 || (l1 == l2 && j1 < j2)));
+}
+
+}  // namespace
+
+// Row ownership: sector row R (points [32R, 32R+32)) lives in cluster CTA
+// R % CS as its local row R / CS, and inside the CTA in warp (R / CS) % W.
+// Interleaving matters: on axis-sorted clouds the rows near the pivot are
+// contiguous, so contiguous chunks would hand one CTA (one warp) all the work.
+template <typename CT, int W, int RPL, int CS, bool WINDOWED>
+__global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const long long flat = static_cast<long long>(blockIdx.x) / CS;  // one sector per cluster
+  const long long b = flat / p.M, s = flat % p.M;
+  const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+  const int n = g.n;
+  const int srows = (n + 31) >> 5;                          // sector rows
+  const int rows = srows > rank ? (srows - rank + CS - 1) / CS : 0;  // local rows
+  const int np = (((p.nmax + 31) >> 5) + kRowsPad) << 5;   // local capacity
+  double* d = reinterpret_cast<double*>(smem);
+  CT* xs = reinterpret_cast<CT*>(d + np);
+  CT* ys = xs + np;
+  CT* zs = ys + np;
+  unsigned* sampled = reinterpret_cast<unsigned*>(zs + np);
+  uint4* cand = reinterpret_cast<uint4*>(sampled + (np >> 5) + 4 - ((np >> 5) & 3));
+  Cand* xbuf = reinterpret_cast<Cand*>(cand + 2 * W);  // [2][CS]
+  if (sizeof(CT) < sizeof(double) && p.f64) __trap();
+  // local point jl <-> sector point ((jl / 32) * CS + rank) * 32 + jl % 32
+  auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
+  auto to_local = [&](int gj) { return (((gj >> 5) / CS) << 5) + (gj & 31); };
+
+  {
+    const long long cloud = (b * p.N + g.begin) * 3;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int jl = threadIdx.x; jl < np; jl += W * 32) {
+      const int gj = to_sector(jl);
+      const bool valid = (jl >> 5) < rows && gj < n;
+      double x = 0, y = 0, z = 0;
+      if (valid) {
+        if (p.f64) {
+          const double* q = static_cast<const double*>(p.xyz) + cloud + 3LL * gj;
+          x = q[0]; y = q[1]; z = q[2];
+        } else {
+          const float* q = static_cast<const float*>(p.xyz) + cloud + 3LL * gj;
+          x = q[0]; y = q[1]; z = q[2];
+        }
+      }
+      xs[jl] = static_cast<CT>(x);
+      ys[jl] = static_cast<CT>(y);
+      zs[jl] = static_cast<CT>(z);
+      d[jl] = valid ? kInf : 0.0;
+    }
+  }
+  for (int w = threadIdx.x; w < (np >> 5); w += W * 32) sampled[w] = 0u;
+  if (p.out_sector && rank == 0)
+    for (int i = threadIdx.x; i < g.quota; i += W * 32)
+      p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
+  __syncthreads();
+
+  // per-lane row metadata: local rows r = warp + W * (lane + 32 * i)
+  float bx0[RPL], bx1[RPL], by0[RPL], by1[RPL], bz0[RPL], bz1[RPL], rmf[RPL];
+  uint32_t rmh[RPL], rml[RPL], rmj[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = warp + W * (lane + 32 * i);
+    float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY, z0 = INFINITY,
+          z1 = -INFINITY;
+    const int R = r * CS + rank;
+    if (r < rows) {
+      const int e = min(32, n - R * 32);
+      for (int q = 0; q < e; ++q) {
+        const int jl = r * 32 + q;
+        x0 = fminf(x0, f_lo(xs[jl]));
+        x1 = fmaxf(x1, f_hi(xs[jl]));
+        y0 = fminf(y0, f_lo(ys[jl]));
+        y1 = fmaxf(y1, f_hi(ys[jl]));
+        z0 = fminf(z0, f_lo(zs[jl]));
+        z1 = fmaxf(z1, f_hi(zs[jl]));
+      }
+    }
+    bx0[i] = x0; bx1[i] = x1; by0[i] = y0; by1[i] = y1; bz0[i] = z0; bz1[i] = z1;
+    rmh[i] = r < rows ? kInfHi : 0u;
+    rml[i] = 0u;
+    rmj[i] = r < rows ? static_cast<uint32_t>(R * 32) : kNoIndex;
+    rmf[i] = r < rows ? INFINITY : -1.0f;
+  }
+
+  GroupSetup gs;
+  gs.b = b;
+  gs.s = s;
+  gs.g = g;
+  int cur = first_point(p, gs);  // sector-local
+  double px, py, pz;
+  {
+    const long long at = (b * p.N + g.begin + cur) * 3;
+    if (p.f64) {
+      const double* q = static_cast<const double*>(p.xyz) + at;
+      px = q[0]; py = q[1]; pz = q[2];
+    } else {
+      const float* q = static_cast<const float*>(p.xyz) + at;
+      px = q[0]; py = q[1]; pz = q[2];
+    }
+  }
+  const long long out_base = b * p.C + g.out_off;
+  const long long index_off = g.begin + p.index_base;
+  if (rank == 0 && threadIdx.x == 0) {
+    if (p.idx64) static_cast<long long*>(p.out_idx)[out_base] = index_off + cur;
+    else static_cast<int*>(p.out_idx)[out_base] = static_cast<int>(index_off + cur);
+  }
+  if (((cur >> 5) % CS) == rank && threadIdx.x == 0) {
+    const int jl = to_local(cur);
+    sampled[jl >> 5] |= 1u << (jl & 31);
+  }
+  const long long K = p.K;
+  const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
+  unsigned writes = 0;
+  unsigned long long evals = 0;
+  int round = 0;
+
+  for (int it = 1; it < g.quota; ++it) {
+    // window, sector-local (full window: everything)
+    int wb = 0, we = n;
+    if constexpr (WINDOWED) {
+      wb = cur >= half_down ? cur - half_down : 0;
+      we = min(n, cur + half_up);
+      evals += static_cast<unsigned long long>(we - wb);
+    }
+    const float pxl = f_lo(px), pxh = f_hi(px), pyl = f_lo(py), pyh = f_hi(py),
+                pzl = f_lo(pz), pzh = f_hi(pz);
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = warp + W * (lane + 32 * i);
+      bool need = r < rows;
+      if constexpr (WINDOWED) {
+        const int R = r * CS + rank;
+        need = need && (R * 32 < we) && (R * 32 + 32 > wb);
+      }
+      if (need) {
+        const float lb = __fadd_rd(__fadd_rd(gap2(bx0[i], bx1[i], pxl, pxh),
+                                             gap2(by0[i], by1[i], pyl, pyh)),
+                                   gap2(bz0[i], bz1[i], pzl, pzh));
+        need = !(__fmul_rd(lb, 0.99999904f) > rmf[i]);
+      }
+      unsigned todo = __ballot_sync(kFull, need);
+      while (todo) {
+        // two rows at a time: loads of both before any store (ILP)
+        const int la = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int lb2 = todo ? __ffs(todo) - 1 : la;
+        todo &= todo ? todo - 1 : 0u;
+        const int ra = warp + W * (la + 32 * i), rb = warp + W * (lb2 + 32 * i);
+        const int ja = (ra << 5) + lane, jb = (rb << 5) + lane;          // local
+        const int ga = ((ra * CS + rank) << 5) + lane, gb = ((rb * CS + rank) << 5) + lane;
+        double da = d[ja], db = d[jb];
+        const double ea = dist2(static_cast<double>(xs[ja]), static_cast<double>(ys[ja]),
+                                static_cast<double>(zs[ja]), px, py, pz);
+        const double eb = dist2(static_cast<double>(xs[jb]), static_cast<double>(ys[jb]),
+                                static_cast<double>(zs[jb]), px, py, pz);
+        const bool wa = ga >= wb && ga < we && ea <= da;
+        const bool wbb = lb2 != la && gb >= wb && gb < we && eb <= db;
+        writes += (wa ? 1u : 0u) + (wbb ? 1u : 0u);
+        if (wa) d[ja] = ea;
+        if (wbb) d[jb] = eb;
+        da = wa ? ea : da;
+        db = wbb ? eb : db;
+        {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(da));
+          const uint32_t h0 = static_cast<uint32_t>(bits >> 32), l0 = static_cast<uint32_t>(bits);
+          const uint32_t h = __reduce_max_sync(kFull, h0);
+          const uint32_t l = __reduce_max_sync(kFull, h0 == h ? l0 : 0u);
+          const uint32_t jj =
+              static_cast<uint32_t>(ga - lane + __ffs(__ballot_sync(kFull, h0 == h && l0 == l)) - 1);
+          if (lane == la) {
+            rmh[i] = h; rml[i] = l; rmj[i] = jj;
+            rmf[i] = __double2float_ru(__hiloint2double(static_cast<int>(h), static_cast<int>(l)));
+          }
+        }
+        {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(db));
+          const uint32_t h0 = static_cast<uint32_t>(bits >> 32), l0 = static_cast<uint32_t>(bits);
+          const uint32_t h = __reduce_max_sync(kFull, h0);
+          const uint32_t l = __reduce_max_sync(kFull, h0 == h ? l0 : 0u);
+          const uint32_t jj =
+              static_cast<uint32_t>(gb - lane + __ffs(__ballot_sync(kFull, h0 == h && l0 == l)) - 1);
+          if (lane == lb2 && lb2 != la) {
+            rmh[i] = h; rml[i] = l; rmj[i] = jj;
+            rmf[i] = __double2float_ru(__hiloint2double(static_cast<int>(h), static_cast<int>(l)));
+          }
+        }
+      }
+    }
+    if (p.trace) {
+      __syncthreads();
+      for (int jl = threadIdx.x; jl < rows * 32; jl += W * 32) {
+        const int gj = to_sector(jl);
+        if (gj < n) p.trace[static_cast<long long>(it - 1) * n + gj] = d[jl];
+      }
+    }
+    // warp -> CTA argmax over the cached row keys (sector-local indices)
+    uint32_t hi = rmh[0], lo = rml[0], j = rmj[0];
+#pragma unroll
+    for (int i = 1; i < RPL; ++i)
+      if (key_gt(rmh[i], rml[i], rmj[i], hi, lo, j)) {
+        hi = rmh[i]; lo = rml[i]; j = rmj[i];
+      }
+    warp_argmax(hi, lo, j);
+    if constexpr (W > 1) {
+      uint4* buf = cand + (round & 1) * W;
+      if (lane == 0) buf[warp] = make_uint4(hi, lo, j, 0);
+      __syncthreads();
+      const uint4 v = lane < W ? buf[lane] : make_uint4(0, 0, kNoIndex, 0);
+      hi = v.x; lo = v.y; j = v.z;
+      warp_argmax(hi, lo, j);
+    }
+    bool zero = (hi | lo) == 0u;
+    if constexpr (CS > 1) {
+      // cluster exchange: every CTA posts (key, index, coords) to every CTA's
+      // slot [round & 1][rank]; one cluster barrier per iteration
+      Cand* slot = xbuf + (round & 1) * CS;
+      if (warp == 0 && lane < CS) {
+        Cand c;
+        c.hi = hi; c.lo = lo; c.j = j; c.pad = 0;
+        const int jl = j == kNoIndex ? 0 : to_local(static_cast<int>(j));
+        c.x = static_cast<double>(xs[jl]); c.y = static_cast<double>(ys[jl]);
+        c.z = static_cast<double>(zs[jl]);
+        cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
+      }
+      cg::this_cluster().sync();
+      uint32_t h = lane < CS ? slot[lane].hi : 0u, l = lane < CS ? slot[lane].lo : 0u;
+      uint32_t jj = lane < CS ? slot[lane].j : kNoIndex;
+      warp_argmax(h, l, jj);
+      zero = (h | l) == 0u;
+      hi = h; lo = l; j = jj;
+      if (!zero) {
+        const unsigned who =
+            __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h && slot[lane].lo == l);
+        const Cand& w = slot[__ffs(who) - 1];
+        px = w.x; py = w.y; pz = w.z;
+      }
+    } else {
+      if (!zero) {
+        px = static_cast<double>(xs[j]); py = static_cast<double>(ys[j]);
+        pz = static_cast<double>(zs[j]);
+      }
+    }
+    ++round;
+    if (zero) {
+      // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
+      uint32_t jm = kNoIndex;
+      for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+        const unsigned free_bits = ~sampled[w];
+        if (free_bits) {
+          const int c = to_sector(w * 32 + __ffs(free_bits) - 1);
+          if (c < n) jm = static_cast<uint32_t>(c);
+        }
+      }
+      jm = __reduce_min_sync(kFull, jm);
+      if constexpr (CS > 1) {
+        Cand* slot = xbuf + (round & 1) * CS;
+        if (warp == 0 && lane < CS) {
+          Cand c{};
+          c.hi = jm != kNoIndex ? 1u : 0u;
+          c.j = jm;
+          const int jl = jm != kNoIndex ? to_local(static_cast<int>(jm)) : 0;
+          c.x = static_cast<double>(xs[jl]); c.y = static_cast<double>(ys[jl]);
+          c.z = static_cast<double>(zs[jl]);
+          cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
+        }
+        cg::this_cluster().sync();
+        uint32_t h = lane < CS ? slot[lane].hi : 0u, l = 0u, jj = lane < CS ? slot[lane].j : kNoIndex;
+        warp_argmax(h, l, jj);
+        const unsigned who = __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h);
+        const Cand& w = slot[__ffs(who) - 1];
+        px = w.x; py = w.y; pz = w.z;
+        j = jj;
+        ++round;
+      } else {
+        j = jm;
+        px = static_cast<double>(xs[j]); py = static_cast<double>(ys[j]);
+        pz = static_cast<double>(zs[j]);
+      }
+    }
+    cur = static_cast<int>(j);  // sector-local
+    if (rank == 0 && threadIdx.x == 0) {
+      if (p.idx64) static_cast<long long*>(p.out_idx)[out_base + it] = index_off + cur;
+      else static_cast<int*>(p.out_idx)[out_base + it] = static_cast<int>(index_off + cur);
+    }
+    if (((cur >> 5) % CS) == rank && threadIdx.x == 0) {
+      const int jl = to_local(cur);
+      sampled[jl >> 5] |= 1u << (jl & 31);
+    }
+  }
+  // stats
+  const unsigned ws = __reduce_add_sync(kFull, writes);
+  if (p.stats) {
+    unsigned long long* st = p.stats + b * 4;
+    if (lane == 0 && ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
+    if (rank == 0 && threadIdx.x == 0) {
+      const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
+      atomicAdd(st + 0, WINDOWED ? evals : iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 3, iters);
+    }
+  }
+  if constexpr (CS > 1) cg::this_cluster().sync();  // keep smem alive for remote writers
+}
+
+template <typename CT>
+size_t rows_smem_bytes(int chunk, int W, int CS) {
+  const size_t np = static_cast<size_t>((((chunk + 31) >> 5) + kRowsPad) << 5);
+  size_t bytes = np * (8 + 3 * sizeof(CT));
+  bytes += ((np >> 5) + 4 - ((np >> 5) & 3)) * 4;  // sampled bits, 16 B aligned
+  bytes += 2 * W * sizeof(uint4);
+  bytes += 2 * CS * sizeof(Cand);
+  return bytes;
+}
+
+template <typename CT, int W, int RPL, int CS, bool WIN>
+cudaError_t launch_rows(SampleParams p, int chunk, cudaStream_t st) {
+  p.nmax = chunk;
+  const size_t smem = rows_smem_bytes<CT>(chunk, W, CS);
+  if (smem > kMaxSmem) return cudaErrorNotSupported;
+  auto kern = rows_kernel<CT, W, RPL, CS, WIN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.B * p.M * CS));
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// Local rows -> warps: about 8 rows per warp (more warps = more rows updated
+// in parallel per iteration), up to 32 warps, then 2 rows per lane.
+template <typename CT, int CS, bool WIN>
+cudaError_t launch_rows_w(SampleParams p, int chunk, cudaStream_t st) {
+  const int rows = (chunk + 31) / 32;
+  if (rows <= 32) return launch_rows<CT, 4, 1, CS, WIN>(p, chunk, st);
+  if (rows <= 64) return launch_rows<CT, 8, 1, CS, WIN>(p, chunk, st);
+  if (rows <= 128) return launch_rows<CT, 16, 1, CS, WIN>(p, chunk, st);
+  if (rows <= 1024) return launch_rows<CT, 32, 1, CS, WIN>(p, chunk, st);
+  return launch_rows<CT, 32, 2, CS, WIN>(p, chunk, st);
+}
+
+template <typename CT, bool WIN>
+cudaError_t launch_rows_cs(SampleParams p, long long n, cudaStream_t st) {
+  // largest chunk that fits shared memory, rounded down to whole rows
+  const int cap = static_cast<int>(((kMaxSmem - 4096) / (8 + 3 * sizeof(CT)) / 32 - kRowsPad) * 32);
+  const long long cs_needed = (n + cap - 1) / cap;
+  int CS = 1;
+  while (CS < cs_needed) CS *= 2;
+  if (CS > 16) return cudaErrorNotSupported;
+  const long long srows = (n + 31) / 32;
+  const int chunk = static_cast<int>((srows + CS - 1) / CS * 32);  // local rows x 32
+  switch (CS) {
+    case 1: return launch_rows_w<CT, 1, WIN>(p, chunk, st);
+    case 2: return launch_rows_w<CT, 2, WIN>(p, chunk, st);
+    case 4: return launch_rows_w<CT, 4, WIN>(p, chunk, st);
+    case 8: return launch_rows_w<CT, 8, WIN>(p, chunk, st);
+    default: return launch_rows_w<CT, 16, WIN>(p, chunk, st);
+  }
+}
+
+cudaError_t run_rows_any(SampleParams p, long long n, bool windowed, cudaStream_t st) {
+  if (p.f64)
+    return windowed ? launch_rows_cs<double, true>(p, n, st) : launch_rows_cs<double, false>(p, n, st);
+  return windowed ? launch_rows_cs<float, true>(p, n, st) : launch_rows_cs<float, false>(p, n, st);
+}
+
+}  // namespace pcsk

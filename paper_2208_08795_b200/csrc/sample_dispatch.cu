@@ -1,4 +1,6 @@
 // Batched sampler entry: picks the kernel family per sector size and window.
+#include <cstdlib>
+
 #include "sampler_common.cuh"
 
 namespace pcsk {
@@ -6,8 +8,12 @@ namespace pcsk {
 cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
                      std::string* msg) {
   p.nmax = static_cast<int>((nmax_sector + 1) & ~1LL);
-  const cudaError_t e = windowed ? run_npdu_any(p, nmax_sector, st)
-                                 : run_full_any(p, nmax_sector, st);
+  // PCS_SAMPLER=rows forces the pruned-row engine (benchmarking / tests)
+  const char* force = std::getenv("PCS_SAMPLER");
+  const bool rows = force && std::string(force) == "rows";
+  cudaError_t e = cudaErrorNotSupported;
+  if (!rows) e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported) e = run_rows_any(p, nmax_sector, windowed, st);
   if (e == cudaErrorNotSupported && msg)
     *msg = "sector of " + std::to_string(nmax_sector) +
            " points exceeds the on-chip samplers of this build";

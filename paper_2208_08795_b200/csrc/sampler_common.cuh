@@ -180,5 +180,6 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // when the sector does not fit the kernel family.
 cudaError_t run_full_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_npdu_any(SampleParams p, long long nmax_sector, cudaStream_t st);
+cudaError_t run_rows_any(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st);
 
 }  // namespace pcsk

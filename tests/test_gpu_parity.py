@@ -222,3 +222,48 @@ def test_determinism_across_calls():
     a = sample(xyz, 2048, method="afps", m=16, sort="x")
     b = sample(xyz, 2048, method="afps", m=16, sort="x")
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_large_sectors_cluster_engine(pcs, oracle):
+    """Sectors beyond one SM's shared memory run on the pruned-row engine over
+    a thread-block cluster (FPS at 16K/32K, NPDU on whole clouds)."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    cases = [(16384, 2048, "fps", 1, None), (32768, 1024, "fps", 1, None),
+             (20000, 3000, "npdu_fps", 1, 65), (40000, 4000, "afps", 4, None),
+             (12000, 1500, "npdu_afps", 1, 129)]
+    for n, c, meth, m, k in cases:
+        xyz = synth.uniform_cube(1, n, n)
+        xyz = synth.stable_sort_np(xyz, 0)[0]
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method=meth, m=m, k=k)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k or 0)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{meth} {n}")
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+    # fp64 input through the drop-in, 10K points (double staging, cluster of 2)
+    pts = synth.random_cloud(10000, 77)
+    got = pcs.fps(pts, 700, seed=3)
+    want = oracle.sample("fps", pts, 700, first="random", seed=3)
+    _same(got, *want)
+
+
+@pytest.mark.parametrize("meth,n,c,m,k", [("fps", 2048, 512, 1, 0), ("afps", 4096, 1024, 4, 0),
+                                          ("npdu_afps", 8192, 2048, 16, 65),
+                                          ("npdu_fps", 3000, 700, 1, 33), ("afps", 700, 90, 3, 0)])
+def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k):
+    """The pruned-row engine on sizes the other kernels normally take
+    (PCS_SAMPLER=rows), including coincident points and random starts."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    monkeypatch.setenv("PCS_SAMPLER", "rows")
+    xyz = synth.stable_sort_np(synth.uniform_cube(3, n, 5), 0)[0]
+    xyz[1, : n // 3] = xyz[1, 0]  # many coincident points
+    for first in ("fixed", "random"):
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method=meth, m=m, k=k or None,
+                         first=first, seed=11)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k, first, 11)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
