@@ -69,6 +69,29 @@ __device__ __forceinline__ void warp_argmax(uint32_t& hi, uint32_t& lo, uint32_t
   j = mj;
 }
 
+// Exact fp32 -> fp64 widening on the integer pipe (F2F.F64.F32 issues on the
+// XU at ~1/4 of the DADD rate and saturates it in the samplers' inner
+// loops). Exact for normal numbers and +-0, which is all the kernels stage
+// for fp32 input (stagers route a sector containing a subnormal to the F2F
+// path; inf/NaN are outside the reference's precondition).
+__device__ __forceinline__ double widen_f32(float f) {
+  const uint32_t b = __float_as_uint(f), a = b & 0x7fffffffu;
+  const uint32_t hi = (a ? (a >> 3) + 0x38000000u : 0u) | (b & 0x80000000u);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(b << 29));
+}
+
+__device__ __forceinline__ bool is_subnormal_f32(float f) {
+  const uint32_t a = __float_as_uint(f) & 0x7fffffffu;
+  return a != 0 && a < 0x00800000u;
+}
+
+// High word of the fp64 value of a non-negative fp32 (subnormals -> 0, a
+// lower bound). Used to compare an fp32 lower bound against an fp64 key.
+__device__ __forceinline__ uint32_t f32_as_f64_hi_lb(float f) {
+  const uint32_t a = __float_as_uint(f) & 0x7fffffffu;
+  return a >= 0x00800000u ? (a >> 3) + 0x38000000u : 0u;
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -122,7 +122,6 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   if (n <= 1024) return run_full<16, 2, true>(p, st);
   if (n <= 2048) return run_full<16, 4, true>(p, st);
   if (n <= 4096) return run_full<16, 8, true>(p, st);
-  if (n <= 8192) return run_full<8, 32, false>(p, st);
   return cudaErrorNotSupported;
 }
 

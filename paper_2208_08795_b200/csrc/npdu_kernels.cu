@@ -18,6 +18,8 @@
 // lanes never write (the window ends inside the sector) and never win the
 // argmax (their d = 0 can only tie a max of 0, which takes the lowest-
 // unsampled path).
+#include <type_traits>
+
 #include "sampler_common.cuh"
 
 namespace pcsk {
@@ -37,8 +39,7 @@ __host__ __device__ __forceinline__ size_t npdu_warp_bytes(int nmax, int rmax) {
 }
 
 // (max d, min index) of row r. Within a row the index grows with the lane,
-// so the lowest lane holding the max is the winner: two reductions and a
-// ballot instead of three reductions.
+// so the lowest lane holding the max is the winner.
 __device__ __forceinline__ void row_key(double dj, int r, uint32_t& hi, uint32_t& lo,
                                         uint32_t& j) {
   const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(dj));
@@ -50,6 +51,11 @@ __device__ __forceinline__ void row_key(double dj, int r, uint32_t& hi, uint32_t
   lo = ml;
   j = static_cast<uint32_t>((r << 5) + __ffs(cand) - 1);
 }
+
+template <bool F2F>
+__device__ __forceinline__ double to_f64(float v) { return F2F ? static_cast<double>(v) : widen_f32(v); }
+template <bool F2F>
+__device__ __forceinline__ double to_f64(double v) { return v; }
 
 template <int RPL>
 __device__ __forceinline__ void store_row(int r, int lane, uint32_t hi, uint32_t lo, uint32_t j,
@@ -99,6 +105,7 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   }
   const int rows = (n + 31) >> 5;
   for (int w = lane; w < (np >> 5); w += 32) sampled[w] = 0u;
+
   if (p.out_sector)
     for (int i = lane; i < g.quota; i += 32)
       p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
@@ -134,9 +141,11 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   unsigned long long evals = 0;
   double* const trace = p.trace;
 
+  auto iterate = [&](auto f2f_tag) {
+  constexpr bool F2F = decltype(f2f_tag)::value;
   for (int it = 1; it < g.quota; ++it) {
-    const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
-                 pz = static_cast<double>(zs[cur]);
+    const double px = to_f64<F2F>(xs[cur]), py = to_f64<F2F>(ys[cur]),
+                 pz = to_f64<F2F>(zs[cur]);
     const int wb = cur >= half_down ? cur - half_down : 0;
     const int we = min(n, cur + half_up);
     evals += static_cast<unsigned long long>(we - wb);
@@ -149,8 +158,8 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
       for (int q = 0; q < RMAX; ++q) {
         const int j = j0 + 32 * q;
         dj[q] = d[j];
-        dist[q] = dist2(static_cast<double>(xs[j]), static_cast<double>(ys[j]),
-                        static_cast<double>(zs[j]), px, py, pz);
+        dist[q] = dist2(to_f64<F2F>(xs[j]), to_f64<F2F>(ys[j]),
+                        to_f64<F2F>(zs[j]), px, py, pz);
       }
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
@@ -173,10 +182,10 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
       for (int r = r_lo; r <= r_hi; r += 2) {
         const int ja = (r << 5) + lane, jb = ja + 32;
         double da = d[ja], db = d[jb];
-        const double ea = dist2(static_cast<double>(xs[ja]), static_cast<double>(ys[ja]),
-                                static_cast<double>(zs[ja]), px, py, pz);
-        const double eb = dist2(static_cast<double>(xs[jb]), static_cast<double>(ys[jb]),
-                                static_cast<double>(zs[jb]), px, py, pz);
+        const double ea = dist2(to_f64<F2F>(xs[ja]), to_f64<F2F>(ys[ja]),
+                                to_f64<F2F>(zs[ja]), px, py, pz);
+        const double eb = dist2(to_f64<F2F>(xs[jb]), to_f64<F2F>(ys[jb]),
+                                to_f64<F2F>(zs[jb]), px, py, pz);
         const bool la = ja >= wb && ja < we && ea <= da;
         const bool lb = jb >= wb && jb < we && eb <= db;
         writes += (la ? 1u : 0u) + (lb ? 1u : 0u);
@@ -226,6 +235,11 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
     }
     __syncwarp();
   }
+  };
+  // F2F widening here: this kernel is latency-bound and F2F's latency is
+  // shorter than the integer widening chain (measured; the XU is not
+  // saturated at NPDU's evaluation rate)
+  iterate(std::true_type{});
   const unsigned ws = __reduce_add_sync(kFull, writes);
   if (p.stats && lane == 0) {
     unsigned long long* st = p.stats + b * 4;

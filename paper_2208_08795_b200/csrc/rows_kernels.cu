@@ -27,6 +27,8 @@
 // dist_writes counts actual writes, which skipped rows provably have none of.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "sampler_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -38,9 +40,15 @@ namespace {
 constexpr int kRowsPad = 2;  // zero rows after each chunk (pair processing)
 
 struct Cand {
-  uint32_t hi, lo, j, pad;
+  uint32_t hi, lo, j;
+  float fx, fy, fz, pad0, pad1;
   double x, y, z;
 };
+
+template <bool F2F>
+__device__ __forceinline__ double to_f64(float v) { return F2F ? static_cast<double>(v) : widen_f32(v); }
+template <bool F2F>
+__device__ __forceinline__ double to_f64(double v) { return v; }
 
 __device__ __forceinline__ float f_lo(float v) { return v; }
 __device__ __forceinline__ float f_hi(float v) { return v; }
@@ -115,10 +123,17 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
   if (p.out_sector && rank == 0)
     for (int i = threadIdx.x; i < g.quota; i += W * 32)
       p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
-  __syncthreads();
+  // fp32 subnormals cannot take the integer widening path (see widen_f32)
+  bool sub_local = false;
+  if constexpr (sizeof(CT) == 4)
+    for (int jl = threadIdx.x; jl < np; jl += W * 32)
+      sub_local |= is_subnormal_f32(static_cast<float>(xs[jl])) ||
+                   is_subnormal_f32(static_cast<float>(ys[jl])) ||
+                   is_subnormal_f32(static_cast<float>(zs[jl]));
+  const bool any_sub = __syncthreads_or(sub_local) != 0;
 
   // per-lane row metadata: local rows r = warp + W * (lane + 32 * i)
-  float bx0[RPL], bx1[RPL], by0[RPL], by1[RPL], bz0[RPL], bz1[RPL], rmf[RPL];
+  float bx0[RPL], bx1[RPL], by0[RPL], by1[RPL], bz0[RPL], bz1[RPL];
   uint32_t rmh[RPL], rml[RPL], rmj[RPL];
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
@@ -142,7 +157,6 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
     rmh[i] = r < rows ? kInfHi : 0u;
     rml[i] = 0u;
     rmj[i] = r < rows ? static_cast<uint32_t>(R * 32) : kNoIndex;
-    rmf[i] = r < rows ? INFINITY : -1.0f;
   }
 
   GroupSetup gs;
@@ -151,6 +165,7 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
   gs.g = g;
   int cur = first_point(p, gs);  // sector-local
   double px, py, pz;
+  float pfx = 0.f, pfy = 0.f, pfz = 0.f;  // exact fp32 pivot (fp32 input only)
   {
     const long long at = (b * p.N + g.begin + cur) * 3;
     if (p.f64) {
@@ -158,7 +173,8 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       px = q[0]; py = q[1]; pz = q[2];
     } else {
       const float* q = static_cast<const float*>(p.xyz) + at;
-      px = q[0]; py = q[1]; pz = q[2];
+      pfx = q[0]; pfy = q[1]; pfz = q[2];
+      px = pfx; py = pfy; pz = pfz;
     }
   }
   const long long out_base = b * p.C + g.out_off;
@@ -177,6 +193,8 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
   unsigned long long evals = 0;
   int round = 0;
 
+  auto iterate = [&](auto f2f_tag) {
+  constexpr bool F2F = decltype(f2f_tag)::value;
   for (int it = 1; it < g.quota; ++it) {
     // window, sector-local (full window: everything)
     int wb = 0, we = n;
@@ -185,8 +203,13 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       we = min(n, cur + half_up);
       evals += static_cast<unsigned long long>(we - wb);
     }
-    const float pxl = f_lo(px), pxh = f_hi(px), pyl = f_lo(py), pyh = f_hi(py),
-                pzl = f_lo(pz), pzh = f_hi(pz);
+    float pxl, pxh, pyl, pyh, pzl, pzh;
+    if constexpr (sizeof(CT) == 4) {
+      pxl = pxh = pfx; pyl = pyh = pfy; pzl = pzh = pfz;
+    } else {
+      pxl = f_lo(px); pxh = f_hi(px); pyl = f_lo(py); pyh = f_hi(py);
+      pzl = f_lo(pz); pzh = f_hi(pz);
+    }
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = warp + W * (lane + 32 * i);
@@ -199,23 +222,22 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
         const float lb = __fadd_rd(__fadd_rd(gap2(bx0[i], bx1[i], pxl, pxh),
                                              gap2(by0[i], by1[i], pyl, pyh)),
                                    gap2(bz0[i], bz1[i], pzl, pzh));
-        need = !(__fmul_rd(lb, 0.99999904f) > rmf[i]);
+        // skip iff lb * (1 - 2^-20) > row max; compared on fp64 high words
+        need = !(f32_as_f64_hi_lb(__fmul_rd(lb, 0.99999904f)) > rmh[i]);
       }
-      unsigned todo = __ballot_sync(kFull, need);
-      while (todo) {
+      int la = static_cast<int>(__reduce_min_sync(kFull, need ? lane : 32u));
+      while (la < 32) {
         // two rows at a time: loads of both before any store (ILP)
-        const int la = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int lb2 = todo ? __ffs(todo) - 1 : la;
-        todo &= todo ? todo - 1 : 0u;
+        const int lb2r = static_cast<int>(__reduce_min_sync(kFull, (need && lane > la) ? lane : 32u));
+        const int lb2 = lb2r < 32 ? lb2r : la;
         const int ra = warp + W * (la + 32 * i), rb = warp + W * (lb2 + 32 * i);
         const int ja = (ra << 5) + lane, jb = (rb << 5) + lane;          // local
         const int ga = ((ra * CS + rank) << 5) + lane, gb = ((rb * CS + rank) << 5) + lane;
         double da = d[ja], db = d[jb];
-        const double ea = dist2(static_cast<double>(xs[ja]), static_cast<double>(ys[ja]),
-                                static_cast<double>(zs[ja]), px, py, pz);
-        const double eb = dist2(static_cast<double>(xs[jb]), static_cast<double>(ys[jb]),
-                                static_cast<double>(zs[jb]), px, py, pz);
+        const double ea = dist2(to_f64<F2F>(xs[ja]), to_f64<F2F>(ys[ja]), to_f64<F2F>(zs[ja]),
+                                px, py, pz);
+        const double eb = dist2(to_f64<F2F>(xs[jb]), to_f64<F2F>(ys[jb]), to_f64<F2F>(zs[jb]),
+                                px, py, pz);
         const bool wa = ga >= wb && ga < we && ea <= da;
         const bool wbb = lb2 != la && gb >= wb && gb < we && eb <= db;
         writes += (wa ? 1u : 0u) + (wbb ? 1u : 0u);
@@ -228,25 +250,23 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
           const uint32_t h0 = static_cast<uint32_t>(bits >> 32), l0 = static_cast<uint32_t>(bits);
           const uint32_t h = __reduce_max_sync(kFull, h0);
           const uint32_t l = __reduce_max_sync(kFull, h0 == h ? l0 : 0u);
-          const uint32_t jj =
-              static_cast<uint32_t>(ga - lane + __ffs(__ballot_sync(kFull, h0 == h && l0 == l)) - 1);
+          const uint32_t m = __reduce_min_sync(kFull, (h0 == h && l0 == l) ? lane : 32u);
           if (lane == la) {
-            rmh[i] = h; rml[i] = l; rmj[i] = jj;
-            rmf[i] = __double2float_ru(__hiloint2double(static_cast<int>(h), static_cast<int>(l)));
+            rmh[i] = h; rml[i] = l; rmj[i] = static_cast<uint32_t>(ga - lane) + m;
           }
         }
-        {
+        if (lb2 != la) {
           const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(db));
           const uint32_t h0 = static_cast<uint32_t>(bits >> 32), l0 = static_cast<uint32_t>(bits);
           const uint32_t h = __reduce_max_sync(kFull, h0);
           const uint32_t l = __reduce_max_sync(kFull, h0 == h ? l0 : 0u);
-          const uint32_t jj =
-              static_cast<uint32_t>(gb - lane + __ffs(__ballot_sync(kFull, h0 == h && l0 == l)) - 1);
-          if (lane == lb2 && lb2 != la) {
-            rmh[i] = h; rml[i] = l; rmj[i] = jj;
-            rmf[i] = __double2float_ru(__hiloint2double(static_cast<int>(h), static_cast<int>(l)));
+          const uint32_t m = __reduce_min_sync(kFull, (h0 == h && l0 == l) ? lane : 32u);
+          if (lane == lb2) {
+            rmh[i] = h; rml[i] = l; rmj[i] = static_cast<uint32_t>(gb - lane) + m;
           }
         }
+        if (lane == la || lane == lb2) need = false;
+        la = static_cast<int>(__reduce_min_sync(kFull, need ? lane : 32u));
       }
     }
     if (p.trace) {
@@ -273,18 +293,33 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       warp_argmax(hi, lo, j);
     }
     bool zero = (hi | lo) == 0u;
-    if constexpr (CS > 1) {
-      // cluster exchange: every CTA posts (key, index, coords) to every CTA's
-      // slot [round & 1][rank]; one cluster barrier per iteration
-      Cand* slot = xbuf + (round & 1) * CS;
+    auto post = [&](Cand* slot, uint32_t h, uint32_t l, uint32_t jj) {
+      // every CTA posts (key, index, coords) to every CTA's slot [rank]
       if (warp == 0 && lane < CS) {
         Cand c;
-        c.hi = hi; c.lo = lo; c.j = j; c.pad = 0;
-        const int jl = j == kNoIndex ? 0 : to_local(static_cast<int>(j));
-        c.x = static_cast<double>(xs[jl]); c.y = static_cast<double>(ys[jl]);
-        c.z = static_cast<double>(zs[jl]);
+        c.hi = h; c.lo = l; c.j = jj; c.pad0 = c.pad1 = 0.f;
+        const int jl = jj == kNoIndex ? 0 : to_local(static_cast<int>(jj));
+        c.x = to_f64<F2F>(xs[jl]); c.y = to_f64<F2F>(ys[jl]); c.z = to_f64<F2F>(zs[jl]);
+        c.fx = static_cast<float>(sizeof(CT) == 4 ? xs[jl] : CT(0));
+        c.fy = static_cast<float>(sizeof(CT) == 4 ? ys[jl] : CT(0));
+        c.fz = static_cast<float>(sizeof(CT) == 4 ? zs[jl] : CT(0));
         cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
       }
+    };
+    auto take = [&](const Cand& w) {
+      px = w.x; py = w.y; pz = w.z;
+      pfx = w.fx; pfy = w.fy; pfz = w.fz;
+    };
+    auto take_local = [&](uint32_t jj) {
+      px = to_f64<F2F>(xs[jj]); py = to_f64<F2F>(ys[jj]); pz = to_f64<F2F>(zs[jj]);
+      if constexpr (sizeof(CT) == 4) {
+        pfx = static_cast<float>(xs[jj]); pfy = static_cast<float>(ys[jj]);
+        pfz = static_cast<float>(zs[jj]);
+      }
+    };
+    if constexpr (CS > 1) {
+      Cand* slot = xbuf + (round & 1) * CS;
+      post(slot, hi, lo, j);
       cg::this_cluster().sync();
       uint32_t h = lane < CS ? slot[lane].hi : 0u, l = lane < CS ? slot[lane].lo : 0u;
       uint32_t jj = lane < CS ? slot[lane].j : kNoIndex;
@@ -294,14 +329,10 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       if (!zero) {
         const unsigned who =
             __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h && slot[lane].lo == l);
-        const Cand& w = slot[__ffs(who) - 1];
-        px = w.x; py = w.y; pz = w.z;
+        take(slot[__ffs(who) - 1]);
       }
     } else {
-      if (!zero) {
-        px = static_cast<double>(xs[j]); py = static_cast<double>(ys[j]);
-        pz = static_cast<double>(zs[j]);
-      }
+      if (!zero) take_local(j);
     }
     ++round;
     if (zero) {
@@ -317,27 +348,17 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       jm = __reduce_min_sync(kFull, jm);
       if constexpr (CS > 1) {
         Cand* slot = xbuf + (round & 1) * CS;
-        if (warp == 0 && lane < CS) {
-          Cand c{};
-          c.hi = jm != kNoIndex ? 1u : 0u;
-          c.j = jm;
-          const int jl = jm != kNoIndex ? to_local(static_cast<int>(jm)) : 0;
-          c.x = static_cast<double>(xs[jl]); c.y = static_cast<double>(ys[jl]);
-          c.z = static_cast<double>(zs[jl]);
-          cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
-        }
+        post(slot, jm != kNoIndex ? 1u : 0u, 0u, jm);
         cg::this_cluster().sync();
         uint32_t h = lane < CS ? slot[lane].hi : 0u, l = 0u, jj = lane < CS ? slot[lane].j : kNoIndex;
         warp_argmax(h, l, jj);
         const unsigned who = __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h);
-        const Cand& w = slot[__ffs(who) - 1];
-        px = w.x; py = w.y; pz = w.z;
+        take(slot[__ffs(who) - 1]);
         j = jj;
         ++round;
       } else {
         j = jm;
-        px = static_cast<double>(xs[j]); py = static_cast<double>(ys[j]);
-        pz = static_cast<double>(zs[j]);
+        take_local(j);
       }
     }
     cur = static_cast<int>(j);  // sector-local
@@ -350,6 +371,11 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       sampled[jl >> 5] |= 1u << (jl & 31);
     }
   }
+  };
+  if (sizeof(CT) == 4 && any_sub)
+    iterate(std::true_type{});
+  else
+    iterate(std::false_type{});
   // stats
   const unsigned ws = __reduce_add_sync(kFull, writes);
   if (p.stats) {

@@ -267,3 +267,23 @@ def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k
         want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k, first, 11)
         np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
+@pytest.mark.parametrize("engine", ["auto", "rows"])
+def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
+    """fp32 subnormals take the exact F2F widening path; +-0 the integer one."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    if engine == "rows":
+        monkeypatch.setenv("PCS_SAMPLER", "rows")
+    xyz = synth.uniform_cube(2, 3000, 8) * np.float32(1e-36)
+    xyz[0, ::5, 0] = np.float32(3e-41)   # subnormal
+    xyz[0, 1::5, 1] = np.float32(-0.0)
+    xyz[1, ::3, 2] = np.float32(0.0)
+    for meth, m, k in (("npdu_afps", 3, 33), ("afps", 2, 0), ("fps", 1, 0)):
+        idx, st = sample(torch.from_numpy(xyz).cuda(), 600, method=meth, m=m, k=k or None)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, 600, m, k)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=meth)
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
