@@ -124,6 +124,17 @@ class ClockSampler:
                 "samples": len(loaded)}
 
 
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the sampler kernel from the committed ncu
+    --set full summary for this workload (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)[workload]
+        return float(d["dram_bytes"]), d["source"]
+    except (OSError, KeyError, ValueError):
+        return None, "no ncu capture for this workload"
+
+
 def fp64_peak():
     try:
         with open(FP64_PEAK_FILE) as f:
@@ -280,9 +291,12 @@ def main():
     peak, peak_src = fp64_peak()
     flops = 8.0 * evals_per_step
     achieved = flops / (kern_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(args.workload)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if peak else None, "traffic": None,
-                "kernel": "fps_window_kernel" if w["K"] else "fps_full_kernel",
+                "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_hbm_bytes": B * N * 12 + B * C * 4,
+                "kernel": pcs.kernel_family(w["method"], N, w["M"], w["K"]),
                 "kernel_ms": kern_ms, "algorithmic_flops": flops, "peak_source": peak_src,
                 "note": "FP64 flops = 8 x dist_evals (3 sub, 3 mul, 2 add; no FMA); the "
                         "argmax work is not counted"}

@@ -28,11 +28,11 @@ except ImportError as exc:  # pragma: no cover - exercised only when unbuilt
     ) from exc
 
 from ._core import afps, exact_sort, fps, local_fps, npdu_afps, npdu_fps  # noqa: E402
-from .ops import METHODS, sample, sort_axis, sample_host_batch  # noqa: E402
+from .ops import METHODS, kernel_family, sample, sort_axis, sample_host_batch  # noqa: E402
 
 LIB_PATH = _os.path.join(_PKG, "lib", "libpcs_gpu.so")
 
 __all__ = [
     "fps", "afps", "npdu_fps", "npdu_afps", "exact_sort", "local_fps",
-    "sample", "sort_axis", "sample_host_batch", "METHODS", "LIB_PATH",
+    "sample", "sort_axis", "sample_host_batch", "kernel_family", "METHODS", "LIB_PATH",
 ]

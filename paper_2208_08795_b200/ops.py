@@ -106,6 +106,24 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
     return tuple(out)
 
 
+def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
+                  env: Optional[str] = None) -> str:
+    """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
+    the per-sector register kernel for full windows up to 4096 points, the
+    NPDU warp kernel for windows over sectors up to 8192 points, the pruned
+    row engine (one CTA or a cluster) otherwise."""
+    import os
+
+    sectored = method in ("afps", "npdu_afps")
+    nmax = -(-n // (m if sectored else 1))
+    windowed = method in ("npdu_fps", "npdu_afps") and k is not None and k < 2 * nmax - 1
+    if (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows":
+        return "rows_kernel"
+    if windowed:
+        return "npdu_warp_kernel" if nmax <= 8192 else "rows_kernel"
+    return "fps_full_kernel" if nmax <= 4096 else "rows_kernel"
+
+
 def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,
                       k: Optional[int] = None, first: str = "fixed", seed: int = 0,
                       sort: Optional[str] = None, device: str = "cuda"):
