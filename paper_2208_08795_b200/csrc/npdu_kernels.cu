@@ -18,6 +18,7 @@
 // lanes never write (the window ends inside the sector) and never win the
 // argmax (their d = 0 can only tie a max of 0, which takes the lowest-
 // unsampled path).
+#include <cstdlib>
 #include <type_traits>
 
 #include "sampler_common.cuh"
@@ -32,10 +33,13 @@ __host__ __device__ __forceinline__ int npdu_padded(int nmax, int rmax) {
   return (((nmax + 31) >> 5) + npdu_pad_rows(rmax)) << 5;
 }
 
-template <typename CT>
+// GC: xyz stays in global memory (L1/L2-resident input) and only d[] and
+// the bitmap occupy shared memory, which roughly triples the resident
+// sectors per SM at the price of L2 latency on the window's coordinates.
+template <typename CT, bool GC = false>
 __host__ __device__ __forceinline__ size_t npdu_warp_bytes(int nmax, int rmax) {
   const size_t np = static_cast<size_t>(npdu_padded(nmax, rmax));
-  return (np * (8 + 3 * sizeof(CT)) + np / 8 + 15) & ~size_t(15);
+  return (np * (8 + (GC ? 0 : 3 * sizeof(CT))) + np / 8 + 15) & ~size_t(15);
 }
 
 // (max d, min index) of row r. Within a row the index grows with the lane,
@@ -75,8 +79,8 @@ __device__ __forceinline__ void store_row(int r, int lane, uint32_t hi, uint32_t
 // chains, then the stores, then the reductions) so the rows overlap. Rows
 // past the window get no writes and re-reduce to their cached value.
 // RMAX == 0: runtime row loop (wide windows).
-template <typename CT, int RPL, int RMAX>
-__global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
+template <typename CT, int RPL, int RMAX, bool GC>
+__global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long flat = static_cast<long long>(blockIdx.x) * p.G + gid;
@@ -84,14 +88,20 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   const long long b = flat / p.M, s = flat % p.M;
   const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
   const int n = g.n, np = npdu_padded(p.nmax, RMAX);
-  unsigned char* base = smem + static_cast<size_t>(gid) * npdu_warp_bytes<CT>(p.nmax, RMAX);
+  unsigned char* base = smem + static_cast<size_t>(gid) * npdu_warp_bytes<CT, GC>(p.nmax, RMAX);
   double* d = reinterpret_cast<double*>(base);
   CT* xs = reinterpret_cast<CT*>(d + np);
   CT* ys = xs + np;
   CT* zs = ys + np;
-  unsigned* sampled = reinterpret_cast<unsigned*>(zs + np);
+  unsigned* sampled = reinterpret_cast<unsigned*>(GC ? reinterpret_cast<CT*>(d + np) : zs + np);
+  // coordinate fetch: shared SoA, or the global AoS input (clamped into the
+  // sector so pad lanes never read past it)
+  const CT* gsrc = static_cast<const CT*>(p.xyz) + (b * p.N + g.begin) * 3;
+  auto X = [&](int j) -> CT { if constexpr (GC) return __ldg(gsrc + 3 * min(j, n - 1)); else return xs[j]; };
+  auto Y = [&](int j) -> CT { if constexpr (GC) return __ldg(gsrc + 3 * min(j, n - 1) + 1); else return ys[j]; };
+  auto Z = [&](int j) -> CT { if constexpr (GC) return __ldg(gsrc + 3 * min(j, n - 1) + 2); else return zs[j]; };
   if (sizeof(CT) < sizeof(double) && p.f64) __trap();  // fp32 staging is fp32-input only
-  {
+  if constexpr (!GC) {
     const long long off = (b * p.N + g.begin) * 3;
     if (p.f64)
       stage_sector(static_cast<const double*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
@@ -101,7 +111,8 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   for (int j = lane; j < np; j += 32) {
     d[j] = j < n ? kInf : 0.0;
-    if (j >= n) xs[j] = ys[j] = zs[j] = CT(0);
+    if constexpr (!GC)
+      if (j >= n) xs[j] = ys[j] = zs[j] = CT(0);
   }
   const int rows = (n + 31) >> 5;
   for (int w = lane; w < (np >> 5); w += 32) sampled[w] = 0u;
@@ -144,8 +155,7 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   auto iterate = [&](auto f2f_tag) {
   constexpr bool F2F = decltype(f2f_tag)::value;
   for (int it = 1; it < g.quota; ++it) {
-    const double px = to_f64<F2F>(xs[cur]), py = to_f64<F2F>(ys[cur]),
-                 pz = to_f64<F2F>(zs[cur]);
+    const double px = to_f64<F2F>(X(cur)), py = to_f64<F2F>(Y(cur)), pz = to_f64<F2F>(Z(cur));
     const int wb = cur >= half_down ? cur - half_down : 0;
     const int we = min(n, cur + half_up);
     evals += static_cast<unsigned long long>(we - wb);
@@ -158,8 +168,7 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
       for (int q = 0; q < RMAX; ++q) {
         const int j = j0 + 32 * q;
         dj[q] = d[j];
-        dist[q] = dist2(to_f64<F2F>(xs[j]), to_f64<F2F>(ys[j]),
-                        to_f64<F2F>(zs[j]), px, py, pz);
+        dist[q] = dist2(to_f64<F2F>(X(j)), to_f64<F2F>(Y(j)), to_f64<F2F>(Z(j)), px, py, pz);
       }
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
@@ -182,10 +191,8 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
       for (int r = r_lo; r <= r_hi; r += 2) {
         const int ja = (r << 5) + lane, jb = ja + 32;
         double da = d[ja], db = d[jb];
-        const double ea = dist2(to_f64<F2F>(xs[ja]), to_f64<F2F>(ys[ja]),
-                                to_f64<F2F>(zs[ja]), px, py, pz);
-        const double eb = dist2(to_f64<F2F>(xs[jb]), to_f64<F2F>(ys[jb]),
-                                to_f64<F2F>(zs[jb]), px, py, pz);
+        const double ea = dist2(to_f64<F2F>(X(ja)), to_f64<F2F>(Y(ja)), to_f64<F2F>(Z(ja)), px, py, pz);
+        const double eb = dist2(to_f64<F2F>(X(jb)), to_f64<F2F>(Y(jb)), to_f64<F2F>(Z(jb)), px, py, pz);
         const bool la = ja >= wb && ja < we && ea <= da;
         const bool lb = jb >= wb && jb < we && eb <= db;
         writes += (la ? 1u : 0u) + (lb ? 1u : 0u);
@@ -251,17 +258,17 @@ __global__ void __launch_bounds__(512) npdu_warp_kernel(const SampleParams p) {
   }
 }
 
-template <typename CT, int RPL, int RMAX>
+template <typename CT, int RPL, int RMAX, bool GC>
 cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
-  const size_t warp_bytes = npdu_warp_bytes<CT>(p.nmax, RMAX);
+  const size_t warp_bytes = npdu_warp_bytes<CT, GC>(p.nmax, RMAX);
   // warps per CTA: as many as shared memory lets one SM hold (one CTA per SM
   // when the batch is large), but never so many that CTAs < SMs
   const long long per_sm = static_cast<long long>(kMaxSmem / warp_bytes);
   const long long sectors = p.B * p.M;
-  const int G = static_cast<int>(std::max(1LL, std::min({16LL, per_sm, sectors / 148})));
+  const int G = static_cast<int>(std::max(1LL, std::min({24LL, per_sm, sectors / 148})));
   const size_t smem = warp_bytes * G;
   if (smem > kMaxSmem) return cudaErrorNotSupported;
-  auto kern = npdu_warp_kernel<CT, RPL, RMAX>;
+  auto kern = npdu_warp_kernel<CT, RPL, RMAX, GC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -271,26 +278,313 @@ cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <typename CT, int RPL>
+template <typename CT, int RPL, bool GC>
 cudaError_t run_npdu_rows(SampleParams p, cudaStream_t st) {
   // rows a window of K consecutive points can touch: ceil((K + 31) / 32)
   const long long rows_needed = (p.K + 62) / 32;
-  if (rows_needed <= 2) return run_npdu<CT, RPL, 2>(p, st);
-  if (rows_needed <= 3) return run_npdu<CT, RPL, 3>(p, st);
-  if (rows_needed <= 5) return run_npdu<CT, RPL, 5>(p, st);
-  return run_npdu<CT, RPL, 0>(p, st);
+  if (rows_needed <= 2) return run_npdu<CT, RPL, 2, GC>(p, st);
+  if (rows_needed <= 3) return run_npdu<CT, RPL, 3, GC>(p, st);
+  if (rows_needed <= 5) return run_npdu<CT, RPL, 5, GC>(p, st);
+  return run_npdu<CT, RPL, 0, GC>(p, st);
 }
 
 template <int RPL>
 cudaError_t run_npdu_rpl(SampleParams p, cudaStream_t st) {
-  if (p.f64) return run_npdu_rows<double, RPL>(p, st);
+  const char* gc = std::getenv("PCS_NPDU_GC");
+  if (gc && gc[0] == '1') {
+    if (p.f64) return run_npdu_rows<double, RPL, true>(p, st);
+    return run_npdu_rows<float, RPL, true>(p, st);
+  }
+  if (p.f64) return run_npdu_rows<double, RPL, false>(p, st);
   // fp32 input: stage fp32 (widened exactly on use) unless fp64 staging
   // still fits 16 warps per SM
-  if (npdu_warp_bytes<double>(p.nmax, 5) * 16 <= kMaxSmem) return run_npdu_rows<double, RPL>(p, st);
-  return run_npdu_rows<float, RPL>(p, st);
+  if (npdu_warp_bytes<double>(p.nmax, 5) * 16 <= kMaxSmem) return run_npdu_rows<double, RPL, false>(p, st);
+  return run_npdu_rows<float, RPL, false>(p, st);
+}
+
+
+// ---------------------------------------------------------------- TMEM variant
+// Same algorithm, with the fp64 min-distances in tensor memory instead of
+// shared memory: shared memory then holds only xyz (fp32) and the sampled
+// bitmap, so twice as many sectors (= independent dependency chains) fit per
+// SM, and the kernel is latency-bound, so resident sectors are throughput.
+// Layout: warp w of the CTA uses TMEM lanes 32*(w%4).. (its lane quarter)
+// and a column block per warp; row r of its sector (32 points) is the column
+// pair (2r, 2r+1) = (lo, hi) words of each lane's double. A window's RMAX rows
+// are one or two tcgen05.ld/st per iteration.
+
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1]) : "r"(a));
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7]) : "r"(a));
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};"
+               :: "r"(a), "r"(r[0]), "r"(r[1]) : "memory");
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+               :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                  "r"(r[6]), "r"(r[7]) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// RMAX rows = 2*RMAX columns, as power-of-two tcgen05 shapes
+template <int RMAX>
+__device__ __forceinline__ void tm_load_rows(uint32_t a, double (&v)[RMAX]) {
+  static_assert(RMAX == 2 || RMAX == 3 || RMAX == 5, "row count");
+  uint32_t w[2 * RMAX];
+  if constexpr (RMAX == 2) {
+    uint32_t t[4];
+    tm_ld(a, t);
+    tm_wait_ld();
+    for (int i = 0; i < 4; ++i) w[i] = t[i];
+  } else if constexpr (RMAX == 3) {
+    uint32_t t[4], u[2];
+    tm_ld(a, t);
+    tm_ld(a + 4, u);
+    tm_wait_ld();
+    for (int i = 0; i < 4; ++i) w[i] = t[i];
+    w[4] = u[0]; w[5] = u[1];
+  } else {
+    uint32_t t[8], u[2];
+    tm_ld(a, t);
+    tm_ld(a + 8, u);
+    tm_wait_ld();
+    for (int i = 0; i < 8; ++i) w[i] = t[i];
+    w[8] = u[0]; w[9] = u[1];
+  }
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) v[q] = __hiloint2double(static_cast<int>(w[2 * q + 1]), static_cast<int>(w[2 * q]));
+}
+
+template <int RMAX>
+__device__ __forceinline__ void tm_store_rows(uint32_t a, const double (&v)[RMAX]) {
+  uint32_t w[2 * RMAX];
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) {
+    w[2 * q] = static_cast<uint32_t>(__double2loint(v[q]));
+    w[2 * q + 1] = static_cast<uint32_t>(__double2hiint(v[q]));
+  }
+  if constexpr (RMAX == 2) {
+    uint32_t t[4] = {w[0], w[1], w[2], w[3]};
+    tm_st(a, t);
+  } else if constexpr (RMAX == 3) {
+    uint32_t t[4] = {w[0], w[1], w[2], w[3]}, u[2] = {w[4], w[5]};
+    tm_st(a, t);
+    tm_st(a + 4, u);
+  } else {
+    uint32_t t[8] = {w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]}, u[2] = {w[8], w[9]};
+    tm_st(a, t);
+    tm_st(a + 8, u);
+  }
+}
+
+__host__ __device__ __forceinline__ int tm_cols_per_warp(int nmax, int rmax) {
+  return 2 * (((nmax + 31) >> 5) + rmax);
+}
+
+__host__ __device__ __forceinline__ size_t tm_warp_smem(int nmax) {
+  return (size_t(12) * nmax + 4 * ((nmax + 31) / 32 + 8) + 15) & ~size_t(15);
+}
+
+// fp32 input, sectors <= 1024 points (one row maximum per lane)
+template <int RMAX>
+__global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t tm_base_sh;
+  const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (gid == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&tm_base_sh))), "r"(tm_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm_base = tm_base_sh;
+  const long long flat = static_cast<long long>(blockIdx.x) * p.G + gid;
+  if (flat < p.B * p.M) {
+    const long long b = flat / p.M, s = flat % p.M;
+    const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+    const int n = g.n;
+    const int cpw = tm_cols_per_warp(p.nmax, RMAX);
+    // this warp's TMEM: lane quarter (gid % 4), column block (gid / 4)
+    const uint32_t tm = tm_base + ((static_cast<uint32_t>(gid & 3) * 32u) << 16) +
+                        static_cast<uint32_t>((gid >> 2) * cpw);
+    unsigned char* base = smem + static_cast<size_t>(gid) * tm_warp_smem(p.nmax);
+    float* xs = reinterpret_cast<float*>(base);
+    float* ys = xs + p.nmax;
+    float* zs = ys + p.nmax;
+    unsigned* sampled = reinterpret_cast<unsigned*>(zs + p.nmax);
+    stage_sector(static_cast<const float*>(p.xyz) + (b * p.N + g.begin) * 3, n, xs, ys, zs, lane, 32);
+    const int rows = (n + 31) >> 5;
+    for (int w = lane; w < rows + 8; w += 32) sampled[w] = 0u;
+    // d = +inf on the sector, 0 on the pad rows
+    {
+      const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+      for (int r = 0; r < rows + RMAX; ++r) {
+        const int j = (r << 5) + lane;
+        const double v = j < n ? kInf : 0.0;
+        uint32_t t[2] = {static_cast<uint32_t>(__double2loint(v)), static_cast<uint32_t>(__double2hiint(v))};
+        tm_st(tm + 2 * r, t);
+      }
+      tm_wait_st();
+    }
+    if (p.out_sector)
+      for (int i = lane; i < g.quota; i += 32)
+        p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
+    uint32_t rm_hi = lane < rows ? kInfHi : 0u, rm_lo = 0u;
+    uint32_t rm_j = lane < rows ? static_cast<uint32_t>(lane * 32) : kNoIndex;
+    GroupSetup gs;
+    gs.b = b;
+    gs.s = s;
+    gs.g = g;
+    int cur = first_point(p, gs);
+    const long long out_base = b * p.C + g.out_off;
+    const long long index_off = g.begin + p.index_base;
+    int* out32 = static_cast<int*>(p.out_idx) + out_base;
+    long long* out64 = static_cast<long long*>(p.out_idx) + out_base;
+    if (lane == 0) {
+      if (p.idx64) out64[0] = index_off + cur;
+      else out32[0] = static_cast<int>(index_off + cur);
+      sampled[cur >> 5] |= 1u << (cur & 31);
+    }
+    __syncwarp();
+    const long long K = p.K;
+    const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
+    unsigned writes = 0;
+    unsigned long long evals = 0;
+    for (int it = 1; it < g.quota; ++it) {
+      const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
+                   pz = static_cast<double>(zs[cur]);
+      const int wb = cur >= half_down ? cur - half_down : 0;
+      const int we = min(n, cur + half_up);
+      evals += static_cast<unsigned long long>(we - wb);
+      const int r_lo = wb >> 5;
+      const int j0 = (r_lo << 5) + lane;
+      double dj[RMAX], dist[RMAX];
+      tm_wait_st();
+      tm_load_rows<RMAX>(tm + 2 * r_lo, dj);
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int jc = min(j0 + 32 * q, n - 1);
+        dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
+                        static_cast<double>(zs[jc]), px, py, pz);
+      }
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        const int j = j0 + 32 * q;
+        const bool lower = j >= wb && j < we && dist[q] <= dj[q];
+        writes += lower ? 1u : 0u;
+        dj[q] = lower ? dist[q] : dj[q];
+      }
+      tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) {
+        uint32_t hi, lo, jj;
+        row_key(dj[q], r_lo + q, hi, lo, jj);
+        if (r_lo + q == lane) {
+          rm_hi = hi;
+          rm_lo = lo;
+          rm_j = jj;
+        }
+      }
+      if (p.trace) {
+        tm_wait_st();
+        for (int r = 0; r < rows; ++r) {
+          uint32_t t[2];
+          tm_ld(tm + 2 * r, t);
+          tm_wait_ld();
+          const int j = (r << 5) + lane;
+          if (j < n)
+            p.trace[static_cast<long long>(it - 1) * n + j] =
+                __hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0]));
+        }
+      }
+      uint32_t hi = rm_hi, lo = rm_lo, j = rm_j;
+      warp_argmax(hi, lo, j);
+      if ((hi | lo) == 0u) {
+        uint32_t jm = kNoIndex;
+        for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+          const unsigned free_bits = ~sampled[w];
+          if (free_bits) {
+            const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
+            if (cand < static_cast<uint32_t>(n)) jm = cand;
+          }
+        }
+        j = __reduce_min_sync(kFull, jm);
+      }
+      cur = static_cast<int>(j);
+      if (lane == 0) {
+        if (p.idx64) out64[it] = index_off + cur;
+        else out32[it] = static_cast<int>(index_off + cur);
+        sampled[cur >> 5] |= 1u << (cur & 31);
+      }
+      __syncwarp();
+    }
+    tm_wait_st();
+    const unsigned ws = __reduce_add_sync(kFull, writes);
+    if (p.stats && lane == 0) {
+      unsigned long long* st = p.stats + b * 4;
+      const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
+      if (ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
+      atomicAdd(st + 0, evals);
+      atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 3, iters);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (gid == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tm_base), "r"(tm_cols));
+}
+
+template <int RMAX>
+cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
+  const int cpw = tm_cols_per_warp(p.nmax, RMAX);
+  const size_t wsm = tm_warp_smem(p.nmax);
+  const long long sectors = p.B * p.M;
+  // warps per CTA (one CTA per SM): TMEM holds 4 lane quarters x (512 / cpw)
+  // column blocks; shared memory and 32 warps bound it too
+  long long G = std::min<long long>({32, 4LL * (512 / cpw), static_cast<long long>(kMaxSmem / wsm)});
+  G = std::max(1LL, std::min(G, (sectors + 147) / 148));
+  int cols = 32;
+  while (cols < ((G + 3) / 4) * cpw) cols *= 2;
+  if (cols > 512) return cudaErrorNotSupported;
+  const size_t smem = wsm * G;
+  auto kern = npdu_tmem_kernel<RMAX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  p.G = static_cast<int>(G);
+  const long long blocks = (sectors + G - 1) / G;
+  kern<<<static_cast<unsigned>(blocks), static_cast<unsigned>(32 * G), smem, st>>>(p, cols);
+  return cudaGetLastError();
 }
 
 cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
+  const char* tmv = std::getenv("PCS_NPDU_TMEM");
+  const bool use_tmem = !(tmv && tmv[0] == '0');
+  const long long rows_needed = (p.K + 62) / 32;
+  if (use_tmem && !p.f64 && n <= 1024 && rows_needed <= 5) {
+    if (rows_needed <= 2) return run_npdu_tmem<2>(p, st);
+    if (rows_needed <= 3) return run_npdu_tmem<3>(p, st);
+    return run_npdu_tmem<5>(p, st);
+  }
   if (n <= 1024) return run_npdu_rpl<1>(p, st);
   if (n <= 2048) return run_npdu_rpl<2>(p, st);
   if (n <= 4096) return run_npdu_rpl<4>(p, st);

@@ -55,7 +55,11 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
            first: str = "fixed", seed: int = 0, seeds: Optional[torch.Tensor] = None,
            sort: Optional[str] = None, index_dtype: torch.dtype = torch.int32,
            return_sector: bool = False, index_base: int = 0, sector_base: int = 0):
-    """Sample ``c`` points from every cloud of ``xyz`` (CUDA, ``(B, N, 3)``).
+    """Sample ``c`` points from every cloud of ``xyz`` (``(B, N, 3)``).
+
+    CUDA input: stream-ordered on the current stream, results on the device,
+    no synchronisation (CUDA-graph capturable). CPU input (pinned or not):
+    pipelined H2D / compute / D2H, results returned as CPU tensors.
 
     ``method`` is one of fps / afps / npdu_fps / npdu_afps; ``m`` sectors for
     the AFPS variants, ``k`` window for the NPDU variants (the reference's
@@ -75,6 +79,9 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
         raise ValueError(f"unknown method {method!r}")
     if first not in ("fixed", "random"):
         raise ValueError("first must be 'random' or 'fixed'")
+    if isinstance(xyz, torch.Tensor) and not xyz.is_cuda:
+        return _sample_from_host(xyz, c, method, m, k, first, seed, seeds, sort, index_dtype,
+                                 return_sector, index_base, sector_base)
     x = _as_batch(xyz)
     perm = None
     if sort is not None:
@@ -106,6 +113,63 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
     return tuple(out)
 
 
+def _sample_from_host(xyz, c, method, m, k, first, seed, seeds, sort, index_dtype,
+                      return_sector, index_base, sector_base, chunks=None, device=None):
+    """Host batch in, host results out, with the H2D copy of chunk i+1
+    overlapping the sort + sample of chunk i (copy stream + compute stream)
+    and each chunk's results copied back as soon as they are ready. Clouds are
+    independent, so chunking by cloud changes nothing in the results."""
+    x = xyz.unsqueeze(0) if xyz.dim() == 2 else xyz
+    if x.dim() != 3 or x.shape[-1] != 3:
+        raise ValueError("expected an (N, 3) or (B, N, 3) tensor")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError("xyz must be float32 or float64")
+    x = x.contiguous()
+    if not x.is_pinned():
+        x = x.pin_memory()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    B, N = x.shape[0], x.shape[1]
+    if chunks is None:
+        chunks = max(1, min(int(__import__("os").environ.get("PCS_E2E_CHUNKS", "8")), B))
+    bounds = [(i * B) // chunks for i in range(chunks + 1)]
+    xd = torch.empty(x.shape, dtype=x.dtype, device=dev)
+    outs_host = None
+    main = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    copy.wait_stream(main)  # nothing of this call starts before prior work
+    # chunks run concurrently on a few compute streams: one chunk alone does
+    # not fill the GPU, and the copy engine is the bottleneck anyway
+    workers = [torch.cuda.Stream(dev) for _ in range(min(4, chunks))]
+    done = []
+    for i in range(chunks):
+        b0, b1 = bounds[i], bounds[i + 1]
+        if b1 == b0:
+            continue
+        with torch.cuda.stream(copy):
+            xd[b0:b1].copy_(x[b0:b1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        ws = workers[i % len(workers)]
+        ws.wait_event(ev)
+        sd = seeds[b0:b1] if seeds is not None else None
+        with torch.cuda.stream(ws):
+            res = sample(xd[b0:b1], c, method=method, m=m, k=k, first=first, seed=seed,
+                         seeds=sd, sort=sort, index_dtype=index_dtype,
+                         return_sector=return_sector, index_base=index_base,
+                         sector_base=sector_base)
+            if outs_host is None:
+                outs_host = [torch.empty((B,) + tuple(t.shape[1:]), dtype=t.dtype).pin_memory()
+                             for t in res]
+            for h, t in zip(outs_host, res):
+                h[b0:b1].copy_(t, non_blocking=True)
+        done.append(res)  # device results stay alive until the copies finish
+    for ws in workers:
+        main.wait_stream(ws)
+    compute = main
+    compute.synchronize()
+    return tuple(outs_host)
+
+
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None) -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
@@ -127,10 +191,9 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
 def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,
                       k: Optional[int] = None, first: str = "fixed", seed: int = 0,
                       sort: Optional[str] = None, device: str = "cuda"):
-    """Host (numpy) batch in, host results out: H2D copy, sample, D2H copy.
-    The end-to-end path the bench's ``e2e`` figure measures."""
-    arr = np.ascontiguousarray(xyz)
-    host = torch.from_numpy(arr).pin_memory()
-    dev = host.to(device, non_blocking=True)
-    res = sample(dev, c, method=method, m=m, k=k, first=first, seed=seed, sort=sort)
-    return tuple(t.cpu().numpy() for t in res)
+    """Host (numpy) batch in, host (numpy) results out; the pipelined host
+    path of :func:`sample`."""
+    host = torch.from_numpy(np.ascontiguousarray(xyz))
+    with torch.cuda.device(torch.device(device)):
+        res = sample(host, c, method=method, m=m, k=k, first=first, seed=seed, sort=sort)
+    return tuple(t.numpy() for t in res)

@@ -287,3 +287,22 @@ def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
         want_idx, want_st = oracle.sample_batch_f32(meth, xyz, 600, m, k)
         np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=meth)
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
+def test_host_pipelined_path_matches_device_path():
+    """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
+    results as the device path."""
+    import torch
+
+    from paper_2208_08795_b200 import sample, sample_host_batch
+
+    xyz = synth.primitives(10, 4096, 5, seed=2)
+    dev = sample(torch.from_numpy(xyz).cuda(), 1024, method="npdu_afps", m=8, k=65, sort="x",
+                 return_sector=True)
+    host = sample(torch.from_numpy(xyz), 1024, method="npdu_afps", m=8, k=65, sort="x",
+                  return_sector=True)
+    for a, b in zip(dev, host):
+        assert not b.is_cuda
+        np.testing.assert_array_equal(a.cpu().numpy(), b.numpy())
+    npi = sample_host_batch(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
+    np.testing.assert_array_equal(npi[0], dev[0].cpu().numpy())
