@@ -52,6 +52,9 @@ for _n in (2048, 4096, 8192, 16384, 32768):
     WORKLOADS[f"cfg5-npdu-{_n}"] = dict(gen="cube", B=256, N=_n, method="npdu_afps", C=_n // 4,
                                         M=16, K=65, sort="x")
 
+WORKLOADS["cfg5-1m"] = dict(gen="cube", B=1, N=1 << 20, method="afps", C=(1 << 20) // 4, M=1024,
+                            K=None, sort="x")
+
 # latency probes: one NPDU sector per warp, 1 warp / 148 warps / 4096 warps
 for _b in (1, 148, 4096):
     WORKLOADS[f"lat-npdu-{_b}"] = dict(gen="cube", B=_b, N=1024, method="npdu_fps", C=256, M=1,

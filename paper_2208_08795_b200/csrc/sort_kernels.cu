@@ -11,17 +11,25 @@
 //   words with a bitonic network in shared memory. Packing the storage index
 //   into the low bits makes every word unique and orders ties by index, so an
 //   unstable network yields exactly the stable order.
-// * otherwise (fp64 keys, or larger clouds): one CTA per cloud runs an LSD
+// * fp32, 16384 < N <= 262144: the same network over a thread-block cluster
+//   of up to 16 CTAs (16384 words each in shared memory; cross-CTA steps
+//   through DSMEM). Larger fp32 clouds: the network in global (L2) memory,
+//   block-local steps in shared memory, one launch per global step.
+// * fp64 keys (the drop-in path): one CTA per cloud runs an LSD
 //   radix sort, 8-bit digits, over global ping-pong buffers (L2-resident),
 //   with tile-ordered ranking (match.any + per-warp digit counts) so every
 //   pass is stable. Passes whose digit is constant across the cloud are
 //   skipped.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device_common.cuh"
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace pcsk {
 
@@ -164,6 +172,195 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
+
+// ---------------------------------------------------------------- large clouds
+// Bitonic network on packed (orderkey << 32 | index) words, extended past one
+// CTA's shared memory: a cluster of CS CTAs holds CS blocks of kBlk words
+// (clouds up to 16 x 16384 = 262144 points, DSMEM for the steps whose partner
+// is in another CTA), or for larger clouds the words live in global (L2)
+// memory, with block-local steps in shared memory and one launch per global
+// step. Direction of every compare-exchange: ascending iff (i & k) == 0 for
+// the global index i, so all variants compute the same network.
+
+constexpr int kBlk = 16384;
+
+__device__ __forceinline__ unsigned long long pack_word(const float* __restrict__ src, long long N,
+                                                        long long i, int axis) {
+  return i < N ? (static_cast<unsigned long long>(order_key(src[3 * i + axis])) << 32) |
+                     static_cast<unsigned>(i)
+               : ~0ull;
+}
+
+// steps j = j0, j0/2, ..., 1 of stage k over a block of `len` words that
+// starts at global index `base`
+__device__ __forceinline__ void block_steps(unsigned long long* w, int len, long long base,
+                                            long long k, int j0) {
+  for (int j = j0; j > 0; j >>= 1) {
+    for (int i = threadIdx.x; i < len / 2; i += blockDim.x) {
+      const int lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+      const unsigned long long a = w[lo], c = w[hi];
+      if ((a > c) == (((base + lo) & k) == 0)) {
+        w[lo] = c;
+        w[hi] = a;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void block_sort(unsigned long long* w, int len, long long base) {
+  for (long long k = 2; k <= len; k <<= 1) block_steps(w, len, base, k, static_cast<int>(k >> 1));
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kSortThreads)
+    bitonic_cluster_kernel(const float* __restrict__ xyz, long long N, int axis,
+                           float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  extern __shared__ __align__(16) unsigned long long words[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const long long b = blockIdx.x / CS;
+  const long long base = static_cast<long long>(rank) * kBlk;
+  const long long T = static_cast<long long>(CS) * kBlk;
+  const float* src = xyz + b * N * 3;
+  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) words[i] = pack_word(src, N, base + i, axis);
+  __syncthreads();
+  block_sort(words, kBlk, base);
+  for (long long k = 2LL * kBlk; k <= T; k <<= 1) {
+    long long j = k >> 1;
+    for (; j >= kBlk; j >>= 1) {
+      cluster.sync();
+      const int partner = rank ^ static_cast<int>(j / kBlk);
+      if (rank < partner) {
+        unsigned long long* remote = cluster.map_shared_rank(words, partner);
+        for (int i = threadIdx.x; i < kBlk; i += kSortThreads) {
+          const unsigned long long a = words[i], c = remote[i];
+          if ((a > c) == (((base + i) & k) == 0)) {
+            words[i] = c;
+            remote[i] = a;
+          }
+        }
+      }
+    }
+    cluster.sync();
+    block_steps(words, kBlk, base, k, kBlk / 2);
+  }
+  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) {
+    const long long g = base + i;
+    if (g < N) {
+      const int from = static_cast<int>(words[i] & 0xffffffffu);
+      if (out_perm) out_perm[b * N + g] = from;
+      if (dst) gather_point(src, dst, g, from);
+    }
+  }
+  cluster.sync();  // no CTA leaves while a partner may still touch its words
+}
+
+__global__ void pack_kernel(const float* __restrict__ xyz, long long N, long long T, int axis,
+                            unsigned long long* __restrict__ keys) {
+  const long long b = blockIdx.y;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < T; i += 256LL * gridDim.x)
+    keys[b * T + i] = pack_word(xyz + b * N * 3, N, i, axis);
+}
+
+// one CTA per kBlk block: either the full block sort (k0 == 0) or the local
+// steps kBlk/2..1 of stage k0
+__global__ void __launch_bounds__(kSortThreads)
+    block_kernel(unsigned long long* keys, long long T, long long k0) {
+  extern __shared__ __align__(16) unsigned long long words[];
+  const long long b = blockIdx.y;
+  const long long base = static_cast<long long>(blockIdx.x) * kBlk;
+  unsigned long long* g = keys + b * T + base;
+  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) words[i] = g[i];
+  __syncthreads();
+  if (k0 == 0)
+    block_sort(words, kBlk, base);
+  else
+    block_steps(words, kBlk, base, k0, kBlk / 2);
+  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) g[i] = words[i];
+}
+
+__global__ void global_step_kernel(unsigned long long* keys, long long T, long long k, long long j) {
+  const long long b = blockIdx.y;
+  unsigned long long* w = keys + b * T;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < T / 2; i += 256LL * gridDim.x) {
+    const long long lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+    const unsigned long long a = w[lo], c = w[hi];
+    if ((a > c) == ((lo & k) == 0)) {
+      w[lo] = c;
+      w[hi] = a;
+    }
+  }
+}
+
+__global__ void unpack_kernel(const float* __restrict__ xyz, long long N, long long T,
+                              const unsigned long long* __restrict__ keys,
+                              float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  const long long b = blockIdx.y;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < N; i += 256LL * gridDim.x) {
+    const int from = static_cast<int>(keys[b * T + i] & 0xffffffffu);
+    if (out_perm) out_perm[b * N + i] = from;
+    if (out_xyz) gather_point(xyz + b * N * 3, out_xyz + b * N * 3, i, from);
+  }
+}
+
+template <int CS>
+cudaError_t launch_cluster_sort(const float* xyz, long long batch, long long n, int axis,
+                                float* out_xyz, int* out_perm, cudaStream_t st) {
+  auto kern = bitonic_cluster_kernel<CS>;
+  const size_t smem = sizeof(unsigned long long) * kBlk;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * CS));
+  cfg.blockDim = dim3(kSortThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_global_sort(const float* xyz, long long batch, long long n, int axis,
+                               float* out_xyz, int* out_perm, cudaStream_t st) {
+  long long T = kBlk;
+  while (T < n) T <<= 1;
+  unsigned long long* keys = nullptr;
+  cudaError_t e = cudaMallocAsync(&keys, sizeof(unsigned long long) * T * batch, st);
+  if (e != cudaSuccess) return e;
+  const size_t smem = sizeof(unsigned long long) * kBlk;
+  e = cudaFuncSetAttribute(block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+  const dim3 elem_grid(static_cast<unsigned>(std::min<long long>(4 * 148, (T + 255) / 256)),
+                       static_cast<unsigned>(batch));
+  const dim3 blk_grid(static_cast<unsigned>(T / kBlk), static_cast<unsigned>(batch));
+  if (e == cudaSuccess) {
+    pack_kernel<<<elem_grid, 256, 0, st>>>(xyz, n, T, axis, keys);
+    block_kernel<<<blk_grid, kSortThreads, smem, st>>>(keys, T, 0);
+    for (long long k = 2LL * kBlk; k <= T; k <<= 1) {
+      for (long long j = k >> 1; j >= kBlk; j >>= 1)
+        global_step_kernel<<<elem_grid, 256, 0, st>>>(keys, T, k, j);
+      block_kernel<<<blk_grid, kSortThreads, smem, st>>>(keys, T, k);
+    }
+    unpack_kernel<<<elem_grid, 256, 0, st>>>(xyz, n, T, keys, out_xyz, out_perm);
+    e = cudaGetLastError();
+  }
+  const cudaError_t e2 = cudaFreeAsync(keys, st);
+  return e != cudaSuccess ? e : e2;
+}
+
 }  // namespace pcsk
 
 namespace pcs_internal {
@@ -184,6 +381,16 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
         static_cast<const float*>(xyz), n, axis, npow2, static_cast<float*>(out_xyz), out_perm);
     return cudaGetLastError();
   }
+  if (coord_dtype == PCS_DTYPE_F32) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    if (n <= 2 * pcsk::kBlk) return pcsk::launch_cluster_sort<2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 4 * pcsk::kBlk) return pcsk::launch_cluster_sort<4>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 8 * pcsk::kBlk) return pcsk::launch_cluster_sort<8>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 16 * pcsk::kBlk) return pcsk::launch_cluster_sort<16>(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_global_sort(x, batch, n, axis, o, out_perm, stream);
+  }
+  // fp64 keys (drop-in path): LSD radix
   const size_t key_bytes = coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t count = static_cast<size_t>(batch) * static_cast<size_t>(n);
   void* ws = nullptr;

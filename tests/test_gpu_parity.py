@@ -176,7 +176,7 @@ def test_sort_parity(pcs):
     for name, g in load_sort_goldens().items():
         np.testing.assert_array_equal(pcs.exact_sort(g["points"], "xyz"[int(name[-1])]), g["sorted"])
     rng = np.random.default_rng(3)
-    for n in (1, 2, 17, 1000, 16384, 16385, 40000):
+    for n in (1, 2, 17, 1000, 16384, 16385, 40000, 70000, 200000, 300000):
         xyz = np.round(rng.normal(size=(3, n, 3)), 2).astype(np.float32)
         xyz[:, :: 7, 1] = -0.0
         xyz[:, 1:: 7, 1] = 0.0
@@ -306,3 +306,20 @@ def test_host_pipelined_path_matches_device_path():
         np.testing.assert_array_equal(a.cpu().numpy(), b.numpy())
     npi = sample_host_batch(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
     np.testing.assert_array_equal(npi[0], dev[0].cpu().numpy())
+
+
+def test_one_million_point_afps_vs_oracle(oracle):
+    """BASELINE cfg5's single N=2^20 cloud, AFPS M=1024 (1024-point sectors,
+    quota 256) after the GPU axis sort (global-memory bitonic network)."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    n = 1 << 20
+    xyz = synth.uniform_cube(1, n, 2024)
+    idx, st, perm = sample(torch.from_numpy(xyz).cuda(), n // 4, method="afps", m=1024, sort="x")
+    srt, order = synth.stable_sort_np(xyz, 0)
+    np.testing.assert_array_equal(perm.cpu().numpy(), order)
+    want_idx, want_st = oracle.sample_batch_f32("afps", srt, n // 4, 1024, 0)
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+    np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
