@@ -59,21 +59,34 @@ def build(verbose=False):
     os.makedirs(LIBDIR, exist_ok=True)
     os.makedirs(OBJDIR, exist_ok=True)
     hdrs = _headers()
-    objs = []
+    objs, jobs = [], []
     for src in CU_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJDIR, src + ".o")
         objs.append(o)
         if _newer(o, [s] + hdrs):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-warn-spills", "-I", INC, "-c", s, "-o", o], verbose)
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-Xptxas", "-warn-spills", "-I", INC, "-c", s, "-o", o])
     for src in CXX_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJDIR, src + ".o")
         objs.append(o)
         if _newer(o, [s] + hdrs):
-            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-I", INC,
-                  "-I", os.path.join(CUDA, "include"), "-c", s, "-o", o], verbose)
+            jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-I", INC,
+                         "-I", os.path.join(CUDA, "include"), "-c", s, "-o", o])
+    # translation units compile in parallel (template-heavy kernels dominate)
+    procs = []
+    for cmd in jobs:
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, pr in procs if pr.wait() != 0]
+    if failed:
+        for cmd in failed:
+            out = cmd[cmd.index("-o") + 1]
+            if os.path.exists(out):
+                os.remove(out)
+        raise subprocess.CalledProcessError(1, failed[0])
     if _newer(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs], verbose)
     core = core_path()

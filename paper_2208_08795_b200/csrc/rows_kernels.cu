@@ -27,6 +27,7 @@
 // dist_writes counts actual writes, which skipped rows provably have none of.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "sampler_common.cuh"
@@ -433,14 +434,18 @@ cudaError_t launch_rows(SampleParams p, int chunk, cudaStream_t st) {
 
 // Local rows -> warps: about 8 rows per warp (more warps = more rows updated
 // in parallel per iteration), up to 32 warps, then 2 rows per lane.
+// Warps per CTA from the CTA's row count: more warps update more candidate
+// rows in parallel but each adds fixed per-iteration reduction work; 16 was
+// best measured for 128-512 rows (cfg5 FPS 8K/16K, r01 sweep). A CTA never
+// holds more than 512 rows (shared memory caps a chunk at ~11K fp32 points),
+// so one row per lane suffices.
 template <typename CT, int CS, bool WIN>
 cudaError_t launch_rows_w(SampleParams p, int chunk, cudaStream_t st) {
   const int rows = (chunk + 31) / 32;
   if (rows <= 32) return launch_rows<CT, 4, 1, CS, WIN>(p, chunk, st);
   if (rows <= 64) return launch_rows<CT, 8, 1, CS, WIN>(p, chunk, st);
-  if (rows <= 128) return launch_rows<CT, 16, 1, CS, WIN>(p, chunk, st);
-  if (rows <= 1024) return launch_rows<CT, 32, 1, CS, WIN>(p, chunk, st);
-  return launch_rows<CT, 32, 2, CS, WIN>(p, chunk, st);
+  if (rows <= 512) return launch_rows<CT, 16, 1, CS, WIN>(p, chunk, st);
+  return cudaErrorNotSupported;
 }
 
 template <typename CT, bool WIN>
