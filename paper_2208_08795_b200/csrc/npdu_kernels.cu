@@ -561,7 +561,9 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   // warps per CTA (one CTA per SM): TMEM holds 4 lane quarters x (512 / cpw)
   // column blocks; shared memory and 32 warps bound it too
   long long G = std::min<long long>({32, 4LL * (512 / cpw), static_cast<long long>(kMaxSmem / wsm)});
-  G = std::max(1LL, std::min(G, (sectors + 147) / 148));
+  // balance the waves: as many CTAs per wave as SMs, the same warps in each
+  const long long waves = (sectors + 148 * G - 1) / (148 * G);
+  G = std::max(1LL, std::min(G, (sectors + 148 * waves - 1) / (148 * waves)));
   int cols = 32;
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
