@@ -134,6 +134,32 @@ int pcs_local_fps_host(const double* xyz, int64_t n, int64_t sector_begin,
 int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_xyz,
                         int64_t* out_perm);
 
+/* Sample-quality metrics (proj/src/metrics.cpp:16-52),
+ * bit-identical to the reference's: coverage_radius = max over points of the
+ * distance to the nearest sample; separation = min pairwise distance among
+ * the samples. Batched device form: samples (B, c) int32/int64, out (B)
+ * doubles; an out-of-range sample index yields NaN for that cloud. Host form:
+ * one float64 (N, 3) cloud, int64 samples, reference argument checks and
+ * messages ("coverage_radius: sample set is empty", "... index out of
+ * range", "separation: need at least 2 samples"). */
+int pcs_gpu_coverage_radius(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                            int32_t index_dtype, const void* samples, int64_t c, double* out,
+                            void* stream);
+int pcs_gpu_separation(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                       int32_t index_dtype, const void* samples, int64_t c, double* out,
+                       void* stream);
+int pcs_coverage_radius_host(const double* xyz, int64_t n, const int64_t* samples, int64_t c,
+                             double* out);
+int pcs_separation_host(const double* xyz, int64_t n, const int64_t* samples, int64_t c,
+                        double* out);
+
+/* Cloud files (proj/src/io.cpp:32-122). format 0 = xyz_text,
+ * 1 = f32_bin. pcs_read_cloud_host returns N and copies min(N, capacity)
+ * points (call with out_xyz NULL to size), or -1 with the reference's
+ * std::runtime_error message in pcs_last_error(). */
+long long pcs_read_cloud_host(const char* path, int32_t format, double* out_xyz, int64_t capacity);
+int pcs_write_cloud_host(const char* path, int32_t format, const double* xyz, int64_t n);
+
 /* Last error message of the calling thread ("" after success). */
 const char* pcs_last_error(void);
 const char* pcs_status_string(int status);

@@ -59,6 +59,10 @@ class Oracle:
         lib.or_sample_batch_f32.argtypes = [C.c_int, _fp, _u64, _u64, _u64, _u64, _u64,
                                             _u64, C.c_int, _u64, _i64p, _u64p,
                                             C.c_char_p, C.c_size_t]
+        lib.or_coverage_radius.argtypes = [_dp, _u64, _i64p, _u64]
+        lib.or_coverage_radius.restype = C.c_double
+        lib.or_separation.argtypes = [_dp, _i64p, _u64]
+        lib.or_separation.restype = C.c_double
         lib.or_splitmix_next.argtypes = [_u64p]
         lib.or_splitmix_next.restype = _u64
         lib.or_splitmix_below.argtypes = [_u64p, _u64]
@@ -122,6 +126,16 @@ class Oracle:
             raise OracleError(err.value.decode())
         return idx, st
 
+    def coverage_radius(self, pts, samples):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        s = np.ascontiguousarray(samples, dtype=np.int64)
+        return self.lib.or_coverage_radius(_ptr(pts, _dp), len(pts), _ptr(s, _i64p), len(s))
+
+    def separation(self, pts, samples):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        s = np.ascontiguousarray(samples, dtype=np.int64)
+        return self.lib.or_separation(_ptr(pts, _dp), _ptr(s, _i64p), len(s))
+
     def splitmix(self, seed, count):
         s = C.c_uint64(seed)
         return [self.lib.or_splitmix_next(C.byref(s)) for _ in range(count)]
@@ -152,7 +166,67 @@ class Reference:
         lib.ref_sample_batch_f32.argtypes = [C.c_int, _fp, _u64, _u64, _u64, _u64, _u64,
                                              C.c_int, _u64, C.c_uint, _i64p, _u64p, _dp,
                                              C.c_char_p, C.c_size_t]
+        lib.ref_metric.argtypes = [C.c_int, _dp, _u64, _i64p, _u64, _dp, C.c_char_p, C.c_size_t]
+        lib.ref_read_cloud.argtypes = [C.c_char_p, C.c_int, _dp, _u64, C.c_char_p, C.c_size_t]
+        lib.ref_read_cloud.restype = C.c_longlong
+        lib.ref_write_cloud.argtypes = [C.c_char_p, C.c_int, _dp, _u64]
+        lib.ref_run_bench_csv.restype = C.c_longlong
         self.lib = lib
+
+    def metric(self, which, pts, samples):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        s = np.ascontiguousarray(samples, dtype=np.int64)
+        out = np.zeros(1)
+        err = C.create_string_buffer(256)
+        if self.lib.ref_metric(which, _ptr(pts, _dp), len(pts), _ptr(s, _i64p), len(s),
+                               _ptr(out, _dp), err, 256):
+            raise OracleError(err.value.decode())
+        return float(out[0])
+
+    def coverage_radius(self, pts, samples):
+        return self.metric(0, pts, samples)
+
+    def separation(self, pts, samples):
+        return self.metric(1, pts, samples)
+
+    def read_cloud(self, path, fmt):
+        cap = 1 << 22
+        buf = np.zeros((cap, 3))
+        err = C.create_string_buffer(512)
+        n = self.lib.ref_read_cloud(str(path).encode(), 0 if fmt == "xyz_text" else 1,
+                                    _ptr(buf, _dp), cap, err, 512)
+        if n < 0:
+            raise RuntimeError(err.value.decode())
+        return buf[:n].copy()
+
+    def write_cloud(self, path, fmt, pts):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        self.lib.ref_write_cloud(str(path).encode(), 0 if fmt == "xyz_text" else 1,
+                                 _ptr(pts, _dp), len(pts))
+
+    def run_bench_csv(self, methods, clouds, m_values, k_values, c, trials=1, seed=0,
+                      first="random", threads=1, g=40):
+        """clouds: list of float64 (n, 3) arrays (distinct n). Methods are
+        pcs::Method names (rps, fps, afps, npdu-fps, npdu-afps, grid)."""
+        names = ["rps", "fps", "afps", "npdu-fps", "npdu-afps", "grid"]
+        meth = np.array([names.index(m) for m in methods], np.int32)
+        offs, at = [], 0
+        for cl in clouds:
+            offs.append(at)
+            at += len(cl)
+        xyz = np.ascontiguousarray(np.concatenate(clouds), dtype=np.float64)
+        offs = np.array(offs, np.uint64)
+        ns = np.array([len(cl) for cl in clouds], np.uint64)
+        ms, ks = np.array(m_values, np.uint64), np.array(k_values, np.uint64)
+        cap = 1 << 20
+        out = C.create_string_buffer(cap)
+        self.lib.ref_run_bench_csv(
+            meth.ctypes.data_as(C.c_void_p), C.c_uint64(len(meth)), _ptr(xyz, _dp),
+            offs.ctypes.data_as(C.c_void_p), ns.ctypes.data_as(C.c_void_p), C.c_uint64(len(ns)),
+            ms.ctypes.data_as(C.c_void_p), C.c_uint64(len(ms)), ks.ctypes.data_as(C.c_void_p),
+            C.c_uint64(len(ks)), C.c_uint64(c), C.c_uint64(g), C.c_uint64(trials),
+            C.c_uint64(seed), C.c_int(first == "random"), C.c_uint(threads), out, C.c_size_t(cap))
+        return out.value.decode()
 
     def sample(self, method, pts, c, m=1, k=0, first="fixed", seed=0, threads=1):
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)

@@ -237,3 +237,35 @@ int or_sample_batch_f32(int method, const float* xyz, uint64_t batch_lo, uint64_
   free(sec);
   return rc;
 }
+
+/* ------------------------------------------------------------ metrics
+ * proj/src/metrics.cpp:16-52: fill distance and minimum pairwise distance
+ * over the samples, both fp64 squared_dist, sqrt at the end. */
+double or_coverage_radius(const double* xyz, uint64_t n, const int64_t* s, uint64_t c) {
+  double worst = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    double best = INFINITY;
+    for (uint64_t q = 0; q < c; ++q) {
+      const double dx = xyz[3 * i] - xyz[3 * s[q]];
+      const double dy = xyz[3 * i + 1] - xyz[3 * s[q] + 1];
+      const double dz = xyz[3 * i + 2] - xyz[3 * s[q] + 2];
+      const double v = dx * dx + dy * dy + dz * dz;
+      if (v < best) best = v;
+    }
+    if (best > worst) worst = best;
+  }
+  return sqrt(worst);
+}
+
+double or_separation(const double* xyz, const int64_t* s, uint64_t c) {
+  double best = INFINITY;
+  for (uint64_t i = 0; i < c; ++i)
+    for (uint64_t j = i + 1; j < c; ++j) {
+      const double dx = xyz[3 * s[i]] - xyz[3 * s[j]];
+      const double dy = xyz[3 * s[i] + 1] - xyz[3 * s[j] + 1];
+      const double dz = xyz[3 * s[i] + 2] - xyz[3 * s[j] + 2];
+      const double v = dx * dx + dy * dy + dz * dz;
+      if (v < best) best = v;
+    }
+  return sqrt(best);
+}

@@ -19,6 +19,9 @@
 #include <thread>
 #include <vector>
 
+#include "pcs/bench.hpp"
+#include "pcs/io.hpp"
+#include "pcs/metrics.hpp"
 #include "pcs/order.hpp"
 #include "pcs/sampler.hpp"
 
@@ -175,6 +178,75 @@ int ref_sample_batch_f32(int method, const float* xyz, std::uint64_t batch,
     return -1;
   }
   return static_cast<int>(batch);
+}
+
+// coverage_radius / separation (proj/src/metrics.cpp:16-52)
+int ref_metric(int which, const double* xyz, std::uint64_t n, const std::int64_t* samples,
+               std::uint64_t c, double* out, char* err, std::size_t errlen) {
+  try {
+    std::vector<std::size_t> idx(samples, samples + c);
+    const auto cloud = cloud_f64(xyz, n);
+    *out = which == 0 ? pcs::coverage_radius(cloud, idx) : pcs::separation(cloud, idx);
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return 1;
+  }
+}
+
+// read_cloud (proj/src/io.cpp:93-98): returns N (>= 1) and fills xyz (up
+// to cap points), or -1 with the error message.
+long long ref_read_cloud(const char* path, int format, double* xyz, std::uint64_t cap, char* err,
+                         std::size_t errlen) {
+  try {
+    const auto cloud = pcs::read_cloud(path, format == 0 ? pcs::CloudFormat::XyzText
+                                                         : pcs::CloudFormat::F32Bin);
+    for (std::size_t i = 0; i < cloud.size() && i < cap; ++i)
+      for (int a = 0; a < 3; ++a) xyz[3 * i + a] = cloud.points[i][a];
+    return static_cast<long long>(cloud.size());
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return -1;
+  }
+}
+
+int ref_write_cloud(const char* path, int format, const double* xyz, std::uint64_t n) {
+  pcs::write_cloud(cloud_f64(xyz, n), path,
+                   format == 0 ? pcs::CloudFormat::XyzText : pcs::CloudFormat::F32Bin);
+  return 0;
+}
+
+// run_bench + bench_csv (proj/src/bench.cpp:34-136) over caller-provided
+// clouds: cloud i (n_values[i] points) starts at xyz + 3 * offsets[i].
+// Methods as pcs::Method ints. Writes the CSV into out (truncated to cap).
+long long ref_run_bench_csv(const int* methods, std::uint64_t n_methods, const double* xyz,
+                            const std::uint64_t* offsets, const std::uint64_t* n_values,
+                            std::uint64_t n_sizes, const std::uint64_t* m_values,
+                            std::uint64_t n_m, const std::uint64_t* k_values, std::uint64_t n_k,
+                            std::uint64_t c, std::uint64_t g, std::uint64_t trials,
+                            std::uint64_t seed, int random_first, unsigned threads, char* out,
+                            std::size_t cap) {
+  pcs::BenchOptions o;
+  for (std::uint64_t i = 0; i < n_methods; ++i) o.methods.push_back(static_cast<pcs::Method>(methods[i]));
+  o.n_values.assign(n_values, n_values + n_sizes);
+  o.m_values.assign(m_values, m_values + n_m);
+  o.k_values.assign(k_values, k_values + n_k);
+  o.c = c;
+  o.g = g;
+  o.trials = trials;
+  o.seed = seed;
+  o.seed_policy = random_first ? pcs::SeedPolicy::RandomFirstPoint : pcs::SeedPolicy::FixedFirstPoint;
+  o.threads = threads;
+  auto provider = [&](std::size_t n) {
+    for (std::uint64_t i = 0; i < n_sizes; ++i)
+      if (n_values[i] == n) return cloud_f64(xyz + 3 * offsets[i], n);
+    throw std::invalid_argument("no cloud of that size");
+  };
+  const auto rows = pcs::run_bench(o, provider);
+  const std::string csv = pcs::bench_csv(rows);
+  std::strncpy(out, csv.c_str(), cap - 1);
+  out[cap - 1] = 0;
+  return static_cast<long long>(csv.size());
 }
 
 }  // extern "C"

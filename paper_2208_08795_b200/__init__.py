@@ -24,15 +24,18 @@ try:
 except ImportError as exc:  # pragma: no cover - exercised only when unbuilt
     raise ImportError(
         "paper_2208_08795_b200: native extension not built "
-        "(run `python -m paper_2208_08795_b200._build`); there is no CPU fallback"
+        "(run `python paper_2208_08795_b200/_build.py`); there is no CPU fallback"
     ) from exc
 
-from ._core import afps, exact_sort, fps, local_fps, npdu_afps, npdu_fps  # noqa: E402
-from .ops import METHODS, kernel_family, sample, sort_axis, sample_host_batch  # noqa: E402
+from ._core import (afps, coverage_radius, exact_sort, fps, local_fps, npdu_afps,  # noqa: E402
+                    npdu_fps, read_cloud, separation, write_cloud)
+from .ops import (METHODS, kernel_family, quality, sample, sample_host_batch,  # noqa: E402
+                  sort_axis)
 
 LIB_PATH = _os.path.join(_PKG, "lib", "libpcs_gpu.so")
 
 __all__ = [
-    "fps", "afps", "npdu_fps", "npdu_afps", "exact_sort", "local_fps",
+    "fps", "afps", "npdu_fps", "npdu_afps", "exact_sort", "local_fps", "coverage_radius",
+    "separation", "quality", "read_cloud", "write_cloud",
     "sample", "sort_axis", "sample_host_batch", "kernel_family", "METHODS", "LIB_PATH",
 ]

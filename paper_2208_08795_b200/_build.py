@@ -1,6 +1,6 @@
 """In-tree build of the native pieces (no GPU needed; nvcc cross-compiles).
 
-    python -m paper_2208_08795_b200._build        # or __graft_entry__.build()
+    python paper_2208_08795_b200/_build.py        # or __graft_entry__.build()
 
 Outputs (git-ignored, shipped to the GPU box by gpurun's snapshot):
   paper_2208_08795_b200/lib/libpcs_gpu.so  -- sm_100a kernels + C-ABI
@@ -27,8 +27,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SRCS = ["full_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "sample_dispatch.cu",
-           "sort_kernels.cu"]
-CXX_SRCS = ["capi.cpp", "pcs_api.cpp"]
+           "sort_kernels.cu", "metrics_kernels.cu"]
+CXX_SRCS = ["capi.cpp", "pcs_api.cpp", "io.cpp"]
 HEADERS = ["device_common.cuh", "sampler_common.cuh", "internal.h"]
 
 

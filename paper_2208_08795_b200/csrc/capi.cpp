@@ -252,4 +252,68 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
   return rc;
 }
 
+int pcs_gpu_coverage_radius(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                            int32_t index_dtype, const void* samples, int64_t c, double* out,
+                            void* stream) {
+  clear_error();
+  if (c < 1) { set_error("coverage_radius: sample set is empty"); return PCS_ERR_INVALID_ARGUMENT; }
+  const cudaError_t e = launch_metric(0, coord_dtype, xyz, batch, n, index_dtype, samples, c, out,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PCS_OK : cuda_fail(e);
+}
+
+int pcs_gpu_separation(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                       int32_t index_dtype, const void* samples, int64_t c, double* out,
+                       void* stream) {
+  clear_error();
+  if (c < 2) { set_error("separation: need at least 2 samples"); return PCS_ERR_INVALID_ARGUMENT; }
+  const cudaError_t e = launch_metric(1, coord_dtype, xyz, batch, n, index_dtype, samples, c, out,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PCS_OK : cuda_fail(e);
+}
+
+static int metric_host(int which, const double* xyz, int64_t n, const int64_t* samples, int64_t c,
+                       double* out) {
+  clear_error();
+  const char* who = which == 0 ? "coverage_radius" : "separation";
+  // proj/src/metrics.cpp:18-21, 37-40: same checks, same order
+  if (which == 0 && c < 1) { set_error("coverage_radius: sample set is empty"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (which == 1 && c < 2) { set_error("separation: need at least 2 samples"); return PCS_ERR_INVALID_ARGUMENT; }
+  for (int64_t i = 0; i < c; ++i)
+    if (samples[i] < 0 || samples[i] >= n) {
+      set_error(std::string(who) + ": index out of range");
+      return PCS_ERR_INVALID_ARGUMENT;
+    }
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int rc = PCS_OK;
+  {
+    DevBuf dx(st), di(st), dout(st);
+    if ((e = dx.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
+        (e = di.alloc(sizeof(int64_t) * c)) != cudaSuccess ||
+        (e = dout.alloc(sizeof(double))) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dx.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(di.p, samples, sizeof(int64_t) * c, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = launch_metric(which, PCS_DTYPE_F64, dx.p, 1, n, PCS_INDEX_I64, di.p, c,
+                           static_cast<double*>(dout.p), st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(out, dout.p, sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+      rc = cuda_fail(e);
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int pcs_coverage_radius_host(const double* xyz, int64_t n, const int64_t* samples, int64_t c,
+                             double* out) {
+  return metric_host(0, xyz, n, samples, c, out);
+}
+
+int pcs_separation_host(const double* xyz, int64_t n, const int64_t* samples, int64_t c,
+                        double* out) {
+  return metric_host(1, xyz, n, samples, c, out);
+}
+
 }  // extern "C"

@@ -30,6 +30,12 @@ cudaError_t launch_local_fps(const double* xyz, int64_t n, int64_t sb, int64_t s
                              int64_t* out_idx, uint64_t* out_stats, double* trace,
                              cudaStream_t stream, std::string* msg);
 
+// Batched coverage_radius (which = 0) / separation (which = 1): out[b] is
+// the metric of cloud b (NaN when a sample index is out of range).
+cudaError_t launch_metric(int which, int coord_dtype, const void* xyz, int64_t batch, int64_t n,
+                          int index_dtype, const void* idx, int64_t c, double* out,
+                          cudaStream_t stream);
+
 void set_error(const std::string& msg);
 void clear_error();
 

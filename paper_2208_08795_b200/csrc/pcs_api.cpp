@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "pcs/metrics.hpp"
 #include "pcs/order.hpp"
 #include "pcs/point_cloud.hpp"
 #include "pcs/sampler.hpp"
@@ -207,6 +208,28 @@ SampleResult run_sampler(const PointCloud& cloud, const SamplerSpec& spec, unsig
                                   " is not on the GPU sampling path");
   }
   throw std::invalid_argument("run_sampler: unknown method");
+}
+
+// ------------------------------------------------------------ metrics
+namespace {
+double metric(int which, const PointCloud& cloud, std::span<const std::size_t> samples) {
+  std::vector<int64_t> idx(samples.begin(), samples.end());
+  double out = 0;
+  const auto n = static_cast<int64_t>(cloud.size());
+  const int rc = which == 0
+      ? pcs_coverage_radius_host(flat(cloud), n, idx.data(), static_cast<int64_t>(idx.size()), &out)
+      : pcs_separation_host(flat(cloud), n, idx.data(), static_cast<int64_t>(idx.size()), &out);
+  if (rc != PCS_OK) raise(rc);
+  return out;
+}
+}  // namespace
+
+double coverage_radius(const PointCloud& cloud, std::span<const std::size_t> samples) {
+  return metric(0, cloud, samples);
+}
+
+double separation(const PointCloud& cloud, std::span<const std::size_t> samples) {
+  return metric(1, cloud, samples);
 }
 
 // ------------------------------------------------------------ order

@@ -11,6 +11,8 @@
 #include <stdexcept>
 #include <string>
 
+#include "pcs/io.hpp"
+#include "pcs/metrics.hpp"
 #include "pcs/order.hpp"
 #include "pcs/sampler.hpp"
 #include "pcs_gpu.h"
@@ -161,6 +163,69 @@ PYBIND11_MODULE(_core, m) {
         py::arg("points"), py::arg("begin"), py::arg("end"), py::arg("quota"),
         py::arg("k") = py::none(), py::arg("seed") = 0, py::arg("first") = "random",
         py::arg("trace") = false);
+
+  // cloud files (proj/src/io.cpp); runtime_error -> RuntimeError
+  auto format_of = [](const std::string& name) {
+    const auto f = pcs::parse_format(name);
+    if (!f) throw std::invalid_argument("format must be xyz_text or f32_bin");
+    return *f;
+  };
+  m.def("read_cloud",
+        [format_of](const std::string& path, const std::string& format) {
+          const auto f = format_of(format);
+          pcs::PointCloud cloud;
+          {
+            py::gil_scoped_release nogil;
+            cloud = pcs::read_cloud(path, f);
+          }
+          return to_array(cloud);
+        },
+        py::arg("path"), py::arg("format") = "f32_bin");
+  m.def("write_cloud",
+        [format_of](const F64Array& points, const std::string& path, const std::string& format) {
+          const auto f = format_of(format);
+          const pcs::PointCloud cloud = to_cloud(points);
+          py::gil_scoped_release nogil;
+          pcs::write_cloud(cloud, path, f);
+        },
+        py::arg("points"), py::arg("path"), py::arg("format") = "f32_bin");
+
+  // metrics (proj/bindings/pcsample_module.cpp:198-210)
+  auto indices_of = [](const py::array_t<std::int64_t>& a) {
+    const auto v = a.unchecked<1>();
+    std::vector<std::size_t> out;
+    out.reserve(static_cast<std::size_t>(v.shape(0)));
+    for (py::ssize_t i = 0; i < v.shape(0); ++i) {
+      if (v(i) < 0) throw std::invalid_argument("negative index");
+      out.push_back(static_cast<std::size_t>(v(i)));
+    }
+    return out;
+  };
+  m.def("coverage_radius",
+        [indices_of](const F64Array& points, const py::array_t<std::int64_t>& samples) {
+          const pcs::PointCloud cloud = to_cloud(points);
+          const auto idx = indices_of(samples);
+          py::gil_scoped_release nogil;
+          return pcs::coverage_radius(cloud, idx);
+        },
+        py::arg("points"), py::arg("samples"));
+  m.def("separation",
+        [indices_of](const F64Array& points, const py::array_t<std::int64_t>& samples) {
+          const pcs::PointCloud cloud = to_cloud(points);
+          const auto idx = indices_of(samples);
+          py::gil_scoped_release nogil;
+          return pcs::separation(cloud, idx);
+        },
+        py::arg("points"), py::arg("samples"));
+  m.def("metric_device",
+        [](int which, int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n,
+           int index_dtype, std::uintptr_t idx, std::int64_t c, std::uintptr_t out,
+           std::uintptr_t stream) {
+          auto fn = which == 0 ? pcs_gpu_coverage_radius : pcs_gpu_separation;
+          check(fn(coord_dtype, reinterpret_cast<const void*>(xyz), batch, n, index_dtype,
+                   reinterpret_cast<const void*>(idx), c, reinterpret_cast<double*>(out),
+                   reinterpret_cast<void*>(stream)));
+        });
 
   // Raw device-pointer entry points (torch tensors are unwrapped in Python).
   m.def("sample_device",

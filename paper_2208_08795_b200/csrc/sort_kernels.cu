@@ -68,9 +68,10 @@ __global__ void __launch_bounds__(kSortThreads)
   __syncthreads();
   const int half = npow2 >> 1;
   for (int k = 2; k <= npow2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
+    for (int j = k >> 1, lj = __ffs(k) - 2; j > 0; j >>= 1, --lj) {
       for (int i = threadIdx.x; i < half; i += kSortThreads) {
-        const int lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+        // j is a power of two: pair (lo, lo + j) without integer division
+        const int lo = ((i >> lj) << (lj + 1)) | (i & (j - 1)), hi = lo + j;
         const unsigned long long a = words[lo], c = words[hi];
         const bool ascending = (lo & k) == 0;
         if ((a > c) == ascending) {
@@ -195,9 +196,9 @@ __device__ __forceinline__ unsigned long long pack_word(const float* __restrict_
 // starts at global index `base`
 __device__ __forceinline__ void block_steps(unsigned long long* w, int len, long long base,
                                             long long k, int j0) {
-  for (int j = j0; j > 0; j >>= 1) {
+  for (int j = j0, lj = __ffs(j0) - 1; j > 0; j >>= 1, --lj) {
     for (int i = threadIdx.x; i < len / 2; i += blockDim.x) {
-      const int lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+      const int lo = ((i >> lj) << (lj + 1)) | (i & (j - 1)), hi = lo + j;
       const unsigned long long a = w[lo], c = w[hi];
       if ((a > c) == (((base + lo) & k) == 0)) {
         w[lo] = c;
@@ -284,8 +285,9 @@ __global__ void __launch_bounds__(kSortThreads)
 __global__ void global_step_kernel(unsigned long long* keys, long long T, long long k, long long j) {
   const long long b = blockIdx.y;
   unsigned long long* w = keys + b * T;
+  const int lj = __ffsll(j) - 1;
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < T / 2; i += 256LL * gridDim.x) {
-    const long long lo = 2 * j * (i / j) + (i % j), hi = lo + j;
+    const long long lo = ((i >> lj) << (lj + 1)) | (i & (j - 1)), hi = lo + j;
     const unsigned long long a = w[lo], c = w[hi];
     if ((a > c) == ((lo & k) == 0)) {
       w[lo] = c;

@@ -170,6 +170,27 @@ def _sample_from_host(xyz, c, method, m, k, first, seed, seeds, sort, index_dtyp
     return tuple(outs_host)
 
 
+def quality(xyz: torch.Tensor, idx: torch.Tensor):
+    """Batched coverage_radius and separation (the reference's metrics,
+    proj/src/metrics.cpp:16-52, bit-identical) of samples ``idx`` (B, c) in
+    clouds ``xyz`` (B, N, 3), on the device. Returns two float64 (B,) tensors
+    (NaN where an index is out of range; separation needs c >= 2)."""
+    x = _as_batch(xyz)
+    ix = idx.unsqueeze(0) if idx.dim() == 1 else idx
+    ix = ix.to(device=x.device).contiguous()
+    if ix.dtype not in (torch.int32, torch.int64):
+        ix = ix.to(torch.int64)
+    B, N, c = x.shape[0], x.shape[1], ix.shape[1]
+    cov = torch.empty(B, dtype=torch.float64, device=x.device)
+    sep = torch.full((B,), float("nan"), dtype=torch.float64, device=x.device)
+    st = _stream_handle(x.device)
+    cd, idt = (1 if x.dtype == torch.float64 else 0), (1 if ix.dtype == torch.int64 else 0)
+    _core.metric_device(0, cd, x.data_ptr(), B, N, idt, ix.data_ptr(), c, cov.data_ptr(), st)
+    if c >= 2:
+        _core.metric_device(1, cd, x.data_ptr(), B, N, idt, ix.data_ptr(), c, sep.data_ptr(), st)
+    return cov, sep
+
+
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None) -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):

@@ -323,3 +323,107 @@ def test_one_million_point_afps_vs_oracle(oracle):
     want_idx, want_st = oracle.sample_batch_f32("afps", srt, n // 4, 1024, 0)
     np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
     np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
+# ---------------------------------------------------------------- §8(f) rows
+def test_quality_metrics_bit_exact(pcs, reference, oracle):
+    """coverage_radius / separation (proj/src/metrics.cpp:16-52) on the GPU."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    for t in range(6):
+        n = int(rng.integers(10, 3000))
+        pts = synth.random_cloud(n, 70 + t)
+        if t % 2:
+            pts[: n // 3] = pts[0]
+        idx = pcs.npdu_afps(pts, max(2, n // 7), 3, 33, seed=t)[0]
+        assert pcs.coverage_radius(pts, idx) == reference.coverage_radius(pts, idx)
+        assert pcs.separation(pts, idx) == reference.separation(pts, idx)
+        assert pcs.coverage_radius(pts, idx) == oracle.coverage_radius(pts, idx)
+    with pytest.raises(ValueError, match="coverage_radius: sample set is empty"):
+        pcs.coverage_radius(pts, np.zeros(0, np.int64))
+    with pytest.raises(ValueError, match="separation: need at least 2 samples"):
+        pcs.separation(pts, np.zeros(1, np.int64))
+    with pytest.raises(ValueError, match="coverage_radius: index out of range"):
+        pcs.coverage_radius(pts, np.array([0, 10**6]))
+    # batched, device-resident
+    xyz = synth.primitives(4, 2048, 4, seed=3)
+    dx = torch.from_numpy(xyz).cuda()
+    idx, _ = pcs.sample(dx, 512, method="afps", m=8)
+    cov, sep = pcs.quality(dx, idx)
+    for b in range(4):
+        p64 = xyz[b].astype(np.float64)
+        ib = idx[b].cpu().numpy()
+        assert cov[b].item() == reference.coverage_radius(p64, ib)
+        assert sep[b].item() == reference.separation(p64, ib)
+
+
+def test_bench_harness_csv_matches_reference(reference):
+    """run_bench / bench_csv schema and every non-timing column
+    (proj/src/bench.cpp:34-136) against the real reference."""
+    from paper_2208_08795_b200 import harness
+
+    clouds = {n: synth.stable_sort_np(synth.uniform_cube(1, n, n), 0)[0][0].astype(np.float64)
+              for n in (300, 1000)}
+    opts = harness.BenchOptions(methods=["fps", "afps", "npdu-fps", "npdu-afps"],
+                                n_values=[300, 1000], m_values=[1, 4, 400], k_values=[8, 33],
+                                c=120, trials=2, seed=99)
+    mine = harness.bench_csv(harness.run_bench(opts, lambda n: clouds[n]))
+    ref = reference.run_bench_csv(opts.methods, [clouds[300], clouds[1000]], opts.m_values,
+                                  opts.k_values, opts.c, trials=2, seed=99)
+
+    def mask(csv):
+        out = []
+        for line in csv.strip().split("\n"):
+            f = line.split(",")
+            if f[0] != "method":
+                f[6] = "*"
+            out.append(",".join(f))
+        return out
+
+    assert mask(mine) == mask(ref)
+    assert any("allocate_samples: m exceeds sample count" in l for l in mask(mine))
+
+
+def test_cli_sample_flow(pcs, reference, tmp_path):
+    from paper_2208_08795_b200 import cli
+
+    pts = synth.random_cloud(2000, 4)
+    path = tmp_path / "in.bin"
+    pcs.write_cloud(pts, str(path), "f32_bin")
+    out = tmp_path / "idx.txt"
+    assert cli.main(["sample", "--in", str(path), "--method", "npdu-afps", "--c", "256",
+                     "--m", "8", "--k", "17", "--seed", "5", "--out", str(out)]) == 0
+    got = np.loadtxt(out, dtype=np.int64)
+    cloud = reference.read_cloud(path, "f32_bin")
+    want = reference.sample("npdu_afps", cloud, 256, 8, 17, "random", 5)[0]
+    np.testing.assert_array_equal(got, want)
+
+
+def test_cuda_graph_capture_and_replay():
+    """§8(f1): the batched op is stream-ordered and capturable."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = torch.from_numpy(synth.primitives(8, 4096, 5, seed=6)).cuda()
+    ref = sample(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        sample(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")  # warm (attributes set)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = sample(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, out):
+        assert torch.equal(a, b)
+    xyz.copy_(torch.from_numpy(synth.primitives(8, 4096, 5, seed=7)).cuda())
+    g.replay()
+    want = sample(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
+    torch.cuda.synchronize()
+    for a, b in zip(want, out):
+        assert torch.equal(a, b)

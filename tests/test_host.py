@@ -163,3 +163,40 @@ def test_gloo_two_rank_sharding_equals_single_process(oracle):
     np.testing.assert_array_equal(stats, st.astype(np.int64))
     bi, _ = oracle.sample_batch_f32("afps", synth.uniform_cube(5, 300, 3), 64, 4)
     np.testing.assert_array_equal(brows, bi)
+
+
+# ---------------------------------------------------------------- f2: io
+def test_cloud_files_round_trip_and_match_reference(pcs, reference, tmp_path):
+    pts = synth.random_cloud(50, 9)
+    pts[3] = [-0.0, 1e-300, 3.5e38]
+    for fmt in ("xyz_text", "f32_bin"):
+        p = tmp_path / f"c.{fmt}"
+        pcs.write_cloud(pts, str(p), fmt)
+        mine = pcs.read_cloud(str(p), fmt)
+        np.testing.assert_array_equal(mine, reference.read_cloud(p, fmt))
+        q = tmp_path / f"r.{fmt}"
+        reference.write_cloud(q, fmt, pts)
+        assert p.read_bytes() == q.read_bytes()
+    np.testing.assert_array_equal(pcs.read_cloud(str(tmp_path / "c.xyz_text"), "xyz_text"), pts)
+
+
+@pytest.mark.parametrize("content,fmt", [
+    (b"", "xyz_text"), (b"# only a comment\n\n", "xyz_text"), (b"1 2\n", "xyz_text"),
+    (b"1 2 3\n4 5 6 7\n", "xyz_text"), (b"", "f32_bin"), (b"\x00" * 13, "f32_bin")])
+def test_cloud_file_errors_match_reference(pcs, reference, tmp_path, content, fmt):
+    p = tmp_path / "bad"
+    p.write_bytes(content)
+    with pytest.raises(RuntimeError) as mine:
+        pcs.read_cloud(str(p), fmt)
+    with pytest.raises(RuntimeError) as ref:
+        reference.read_cloud(p, fmt)
+    assert str(mine.value) == str(ref.value)
+    with pytest.raises(RuntimeError, match="cannot open"):
+        pcs.read_cloud(str(tmp_path / "missing"), fmt)
+
+
+def test_cli_usage_errors_exit_2():
+    from paper_2208_08795_b200 import cli
+
+    assert cli.main(["sample"]) == 2
+    assert cli.main(["frobnicate"]) == 2
