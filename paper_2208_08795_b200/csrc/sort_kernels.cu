@@ -174,6 +174,152 @@ __global__ void __launch_bounds__(kSortThreads)
 }
 
 
+// Register-resident bitonic for 2048 <= npow2 <= 16384 (one CTA per cloud,
+// 1024 threads, E = npow2 / 1024 words per thread in registers, blocked:
+// thread t holds words t*E .. t*E+E-1). Steps with j < E run in registers,
+// E <= j < 32E through warp shuffles, and only j >= 32E through shared
+// memory with a block barrier -- 15 barrier steps for 16384 words instead of
+// the 105 of the all-shared-memory network.
+template <int E>
+__global__ void __launch_bounds__(kSortThreads)
+    bitonic_reg_kernel(const float* __restrict__ xyz, long long N, int axis,
+                       float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  extern __shared__ __align__(16) unsigned long long words[];
+  constexpr int NP = E * kSortThreads;
+  const long long b = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
+  const float* src = xyz + b * N * 3;
+  unsigned long long x[E];
+  // vector path: whole thread block of points in range and 16-byte aligned
+  const bool vec = E % 4 == 0 && (t + 1) * E <= N && ((b * N) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(xyz) & 15) == 0;
+  if (vec) {
+    // this thread's E points are 3E consecutive floats (16-byte aligned when
+    // E is a multiple of 4): vector loads, then pick the axis
+    float v[3 * E];
+    const float* p = src + 3LL * t * E;
+    if constexpr (E % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < 3 * E / 4; ++q) {
+        const float4 f = reinterpret_cast<const float4*>(p)[q];
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 3 * E; ++q) v[q] = p[q];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float key = axis == 0 ? v[3 * e] : (axis == 1 ? v[3 * e + 1] : v[3 * e + 2]);
+      x[e] = (static_cast<unsigned long long>(order_key(key)) << 32) | static_cast<unsigned>(t * E + e);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = t * E + e;
+      x[e] = i < N ? (static_cast<unsigned long long>(order_key(src[3LL * i + axis])) << 32) |
+                         static_cast<unsigned>(i)
+                   : ~0ull;
+    }
+  }
+  for (int k = 2; k <= NP; k <<= 1) {
+    int j = k >> 1;
+    if (j >= 32 * E) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) words[t * E + e] = x[e];
+      __syncthreads();
+      for (; j >= 32 * E; j >>= 1) {
+        const int lj = __ffs(j) - 1;
+        for (int q = t; q < NP / 2; q += kSortThreads) {
+          const int lo = ((q >> lj) << (lj + 1)) | (q & (j - 1)), hi = lo + j;
+          const unsigned long long a = words[lo], c = words[hi];
+          if ((a > c) == ((lo & k) == 0)) {
+            words[lo] = c;
+            words[hi] = a;
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = words[t * E + e];
+      __syncthreads();
+    }
+    for (; j >= E; j >>= 1) {
+      const int d = j / E;  // partner lane distance
+      // j, k >= E: which half of the pair and the direction depend on the
+      // thread only
+      const bool keep_min = ((t * E & j) == 0) == ((t * E & k) == 0);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const unsigned long long o = __shfl_xor_sync(kFull, x[e], d);
+        x[e] = (o < x[e]) == keep_min ? o : x[e];
+      }
+    }
+#pragma unroll
+    for (int jj = E / 2; jj > 0; jj >>= 1) {
+      if (jj > (k >> 1)) continue;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & jj) continue;
+        const int i = t * E + e;
+        const unsigned long long a = x[e], c = x[e + jj];
+        if ((a > c) == ((i & k) == 0)) {
+          x[e] = c;
+          x[e + jj] = a;
+        }
+      }
+    }
+  }
+  (void)lane;
+  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+  if (vec && (reinterpret_cast<uintptr_t>(out_perm) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out_xyz) & 15) == 0) {
+    // E consecutive outputs: vector stores of the permutation and the points
+    int from[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) from[e] = static_cast<int>(x[e] & 0xffffffffu);
+    if (out_perm) {
+      int4* pp = reinterpret_cast<int4*>(out_perm + b * N + static_cast<long long>(t) * E);
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q) pp[q] = make_int4(from[4 * q], from[4 * q + 1], from[4 * q + 2], from[4 * q + 3]);
+    }
+    if (dst) {
+      float v[3 * E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        v[3 * e] = src[3LL * from[e]];
+        v[3 * e + 1] = src[3LL * from[e] + 1];
+        v[3 * e + 2] = src[3LL * from[e] + 2];
+      }
+      float4* dp = reinterpret_cast<float4*>(dst + 3LL * t * E);
+#pragma unroll
+      for (int q = 0; q < 3 * E / 4; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long i = t * E + e;
+    if (i < N) {
+      const int from = static_cast<int>(x[e] & 0xffffffffu);
+      if (out_perm) out_perm[b * N + i] = from;
+      if (dst) gather_point(src, dst, i, from);
+    }
+  }
+}
+
+template <int E>
+cudaError_t launch_reg_sort(const float* xyz, long long batch, long long n, int axis,
+                            float* out_xyz, int* out_perm, cudaStream_t st) {
+  const size_t smem = sizeof(unsigned long long) * E * kSortThreads;
+  auto kern = bitonic_reg_kernel<E>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(batch), kSortThreads, smem, st>>>(xyz, n, axis, out_xyz, out_perm);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- large clouds
 // Bitonic network on packed (orderkey << 32 | index) words, extended past one
 // CTA's shared memory: a cluster of CS CTAs holds CS blocks of kBlk words
@@ -370,6 +516,14 @@ namespace pcs_internal {
 cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t n, int axis,
                         void* out_xyz, int32_t* out_perm, cudaStream_t stream) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
+  if (coord_dtype == PCS_DTYPE_F32 && n > 1024 && n <= 16384) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    if (n <= 2048) return pcsk::launch_reg_sort<2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 4096) return pcsk::launch_reg_sort<4>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 8192) return pcsk::launch_reg_sort<8>(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_reg_sort<16>(x, batch, n, axis, o, out_perm, stream);
+  }
   if (coord_dtype == PCS_DTYPE_F32 && n <= 16384) {
     int npow2 = 1;
     while (npow2 < n) npow2 <<= 1;
