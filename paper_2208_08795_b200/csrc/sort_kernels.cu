@@ -180,24 +180,30 @@ __global__ void __launch_bounds__(kSortThreads)
 // E <= j < 32E through warp shuffles, and only j >= 32E through shared
 // memory with a block barrier -- 15 barrier steps for 16384 words instead of
 // the 105 of the all-shared-memory network.
-template <int E>
+// CS > 1: the cloud spans a cluster of CS CTAs (global word index
+// rank * NP + local); steps whose partner lives in another CTA (j >= NP) go
+// through DSMEM with cluster barriers.
+template <int E, int CS>
 __global__ void __launch_bounds__(kSortThreads)
     bitonic_reg_kernel(const float* __restrict__ xyz, long long N, int axis,
                        float* __restrict__ out_xyz, int* __restrict__ out_perm) {
   extern __shared__ __align__(16) unsigned long long words[];
   constexpr int NP = E * kSortThreads;
-  const long long b = blockIdx.x;
+  const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const long long b = blockIdx.x / CS;
+  const long long base = static_cast<long long>(rank) * NP;
   const int t = threadIdx.x, lane = t & 31;
   const float* src = xyz + b * N * 3;
   unsigned long long x[E];
   // vector path: whole thread block of points in range and 16-byte aligned
-  const bool vec = E % 4 == 0 && (t + 1) * E <= N && ((b * N) & 3) == 0 &&
+  const long long g0 = base + static_cast<long long>(t) * E;  // first global word
+  const bool vec = E % 4 == 0 && g0 + E <= N && ((b * N) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(xyz) & 15) == 0;
   if (vec) {
     // this thread's E points are 3E consecutive floats (16-byte aligned when
     // E is a multiple of 4): vector loads, then pick the axis
     float v[3 * E];
-    const float* p = src + 3LL * t * E;
+    const float* p = src + 3 * g0;
     if constexpr (E % 4 == 0) {
 #pragma unroll
       for (int q = 0; q < 3 * E / 4; ++q) {
@@ -211,29 +217,49 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const float key = axis == 0 ? v[3 * e] : (axis == 1 ? v[3 * e + 1] : v[3 * e + 2]);
-      x[e] = (static_cast<unsigned long long>(order_key(key)) << 32) | static_cast<unsigned>(t * E + e);
+      x[e] = (static_cast<unsigned long long>(order_key(key)) << 32) | static_cast<unsigned>(g0 + e);
     }
   } else {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int i = t * E + e;
-      x[e] = i < N ? (static_cast<unsigned long long>(order_key(src[3LL * i + axis])) << 32) |
+      const long long i = g0 + e;
+      x[e] = i < N ? (static_cast<unsigned long long>(order_key(src[3 * i + axis])) << 32) |
                          static_cast<unsigned>(i)
                    : ~0ull;
     }
   }
-  for (int k = 2; k <= NP; k <<= 1) {
-    int j = k >> 1;
+  for (long long k = 2; k <= static_cast<long long>(NP) * CS; k <<= 1) {
+    long long j = k >> 1;
     if (j >= 32 * E) {
 #pragma unroll
       for (int e = 0; e < E; ++e) words[t * E + e] = x[e];
+      if constexpr (CS > 1) {
+        if (j >= NP) {
+          // cross-CTA steps: the lower CTA of each pair exchanges in place
+          for (; j >= NP; j >>= 1) {
+            cg::this_cluster().sync();
+            const int partner = rank ^ static_cast<int>(j / NP);
+            if (rank < partner) {
+              unsigned long long* remote = cg::this_cluster().map_shared_rank(words, partner);
+              for (int q = t; q < NP; q += kSortThreads) {
+                const unsigned long long a = words[q], c = remote[q];
+                if ((a > c) == (((base + q) & k) == 0)) {
+                  words[q] = c;
+                  remote[q] = a;
+                }
+              }
+            }
+          }
+          cg::this_cluster().sync();
+        }
+      }
       __syncthreads();
       for (; j >= 32 * E; j >>= 1) {
-        const int lj = __ffs(j) - 1;
+        const int lj = __ffsll(j) - 1;
         for (int q = t; q < NP / 2; q += kSortThreads) {
-          const int lo = ((q >> lj) << (lj + 1)) | (q & (j - 1)), hi = lo + j;
+          const int lo = ((q >> lj) << (lj + 1)) | (q & static_cast<int>(j - 1)), hi = lo + static_cast<int>(j);
           const unsigned long long a = words[lo], c = words[hi];
-          if ((a > c) == ((lo & k) == 0)) {
+          if ((a > c) == (((base + lo) & k) == 0)) {
             words[lo] = c;
             words[hi] = a;
           }
@@ -245,10 +271,10 @@ __global__ void __launch_bounds__(kSortThreads)
       __syncthreads();
     }
     for (; j >= E; j >>= 1) {
-      const int d = j / E;  // partner lane distance
+      const int d = static_cast<int>(j / E);  // partner lane distance
       // j, k >= E: which half of the pair and the direction depend on the
       // thread only
-      const bool keep_min = ((t * E & j) == 0) == ((t * E & k) == 0);
+      const bool keep_min = ((g0 & j) == 0) == ((g0 & k) == 0);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const unsigned long long o = __shfl_xor_sync(kFull, x[e], d);
@@ -261,7 +287,7 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         if (e & jj) continue;
-        const int i = t * E + e;
+        const long long i = g0 + e;
         const unsigned long long a = x[e], c = x[e + jj];
         if ((a > c) == ((i & k) == 0)) {
           x[e] = c;
@@ -279,7 +305,7 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
     for (int e = 0; e < E; ++e) from[e] = static_cast<int>(x[e] & 0xffffffffu);
     if (out_perm) {
-      int4* pp = reinterpret_cast<int4*>(out_perm + b * N + static_cast<long long>(t) * E);
+      int4* pp = reinterpret_cast<int4*>(out_perm + b * N + g0);
 #pragma unroll
       for (int q = 0; q < E / 4; ++q) pp[q] = make_int4(from[4 * q], from[4 * q + 1], from[4 * q + 2], from[4 * q + 3]);
     }
@@ -291,33 +317,51 @@ __global__ void __launch_bounds__(kSortThreads)
         v[3 * e + 1] = src[3LL * from[e] + 1];
         v[3 * e + 2] = src[3LL * from[e] + 2];
       }
-      float4* dp = reinterpret_cast<float4*>(dst + 3LL * t * E);
+      float4* dp = reinterpret_cast<float4*>(dst + 3 * g0);
 #pragma unroll
       for (int q = 0; q < 3 * E / 4; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
+    if constexpr (CS > 1) cg::this_cluster().sync();
     return;
   }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const long long i = t * E + e;
+    const long long i = g0 + e;
     if (i < N) {
       const int from = static_cast<int>(x[e] & 0xffffffffu);
       if (out_perm) out_perm[b * N + i] = from;
       if (dst) gather_point(src, dst, i, from);
     }
   }
+  if constexpr (CS > 1) cg::this_cluster().sync();  // partners may still read our words
 }
 
-template <int E>
+template <int E, int CS = 1>
 cudaError_t launch_reg_sort(const float* xyz, long long batch, long long n, int axis,
                             float* out_xyz, int* out_perm, cudaStream_t st) {
   const size_t smem = sizeof(unsigned long long) * E * kSortThreads;
-  auto kern = bitonic_reg_kernel<E>;
+  auto kern = bitonic_reg_kernel<E, CS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<static_cast<unsigned>(batch), kSortThreads, smem, st>>>(xyz, n, axis, out_xyz, out_perm);
-  return cudaGetLastError();
+  if (CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * CS));
+  cfg.blockDim = dim3(kSortThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- large clouds
@@ -540,10 +584,11 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   if (coord_dtype == PCS_DTYPE_F32) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
-    if (n <= 2 * pcsk::kBlk) return pcsk::launch_cluster_sort<2>(x, batch, n, axis, o, out_perm, stream);
-    if (n <= 4 * pcsk::kBlk) return pcsk::launch_cluster_sort<4>(x, batch, n, axis, o, out_perm, stream);
-    if (n <= 8 * pcsk::kBlk) return pcsk::launch_cluster_sort<8>(x, batch, n, axis, o, out_perm, stream);
-    if (n <= 16 * pcsk::kBlk) return pcsk::launch_cluster_sort<16>(x, batch, n, axis, o, out_perm, stream);
+    // register network across a cluster of 16384-word CTAs
+    if (n <= 2 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 4 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 4>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 8 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 8>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 16 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 16>(x, batch, n, axis, o, out_perm, stream);
     return pcsk::launch_global_sort(x, batch, n, axis, o, out_perm, stream);
   }
   // fp64 keys (drop-in path): LSD radix
