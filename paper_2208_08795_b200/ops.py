@@ -192,7 +192,7 @@ def quality(xyz: torch.Tensor, idx: torch.Tensor):
 
 
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
-                  env: Optional[str] = None) -> str:
+                  env: Optional[str] = None, dtype: str = "float32") -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
     the per-sector register kernel for full windows up to 4096 points, the
     NPDU warp kernel for windows over sectors up to 8192 points, the pruned
@@ -205,6 +205,9 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     if (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows":
         return "rows_kernel"
     if windowed:
+        if nmax <= 1024 and (k + 62) // 32 <= 5 and dtype != "float64" and \
+                os.environ.get("PCS_NPDU_TMEM", "1") != "0":
+            return "npdu_tmem_kernel"
         return "npdu_warp_kernel" if nmax <= 8192 else "rows_kernel"
     return "fps_full_kernel" if nmax <= 4096 else "rows_kernel"
 
