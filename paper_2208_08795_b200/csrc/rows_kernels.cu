@@ -19,9 +19,10 @@
 //      the update window, proj/src/sectors.cpp:53-61.)
 //   2. the surviving rows are updated exactly (fp64, reference operation
 //      order, `dist <= d` rule) and re-reduced (2 redux + ballot);
-//   3. warp -> CTA (shared memory, one barrier) -> cluster (DSMEM stores, one
-//      cluster barrier) argmax on (max d, min index); candidates carry their
-//      coordinates so the next pivot needs no lookup.
+//   3. warp -> CTA (shared memory, one barrier) -> cluster (DSMEM stores and
+//      remote mbarrier arrivals; no cluster-wide barrier in the loop) argmax
+//      on (max d, min index); candidates carry their coordinates so the next
+//      pivot needs no lookup.
 // dist_evals / argmax_scans / iterations are the reference's counts (the
 // whole window is "evaluated" in its accounting: sampler.cpp:129, 155);
 // dist_writes counts actual writes, which skipped rows provably have none of.
@@ -45,6 +46,27 @@ struct Cand {
   float fx, fy, fz, pad0, pad1;
   double x, y, z;
 };
+
+// Cluster exchange without a cluster-wide barrier: each CTA stores its
+// candidate into every CTA's slot and arrives (release, cluster scope) on
+// that CTA's mbarrier for the round; each CTA waits (acquire) on its own.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+               :: "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, int target_rank) {
+  unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(local_bar)), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(target_rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred done;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
 
 template <bool F2F>
 __device__ __forceinline__ double to_f64(float v) { return F2F ? static_cast<double>(v) : widen_f32(v); }
@@ -93,6 +115,7 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
   unsigned* sampled = reinterpret_cast<unsigned*>(zs + np);
   uint4* cand = reinterpret_cast<uint4*>(sampled + (np >> 5) + 4 - ((np >> 5) & 3));
   Cand* xbuf = reinterpret_cast<Cand*>(cand + 2 * W);  // [2][CS]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * CS);  // [2] mbarriers
   if (sizeof(CT) < sizeof(double) && p.f64) __trap();
   // local point jl <-> sector point ((jl / 32) * CS + rank) * 32 + jl % 32
   auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
@@ -131,7 +154,13 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       sub_local |= is_subnormal_f32(static_cast<float>(xs[jl])) ||
                    is_subnormal_f32(static_cast<float>(ys[jl])) ||
                    is_subnormal_f32(static_cast<float>(zs[jl]));
+  if (CS > 1 && threadIdx.x == 0) {
+    mbar_init(&xbar[0], CS);
+    mbar_init(&xbar[1], CS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const bool any_sub = __syncthreads_or(sub_local) != 0;
+  if constexpr (CS > 1) cg::this_cluster().sync();  // every CTA's barriers exist
 
   // per-lane row metadata: local rows r = warp + W * (lane + 32 * i)
   float bx0[RPL], bx1[RPL], by0[RPL], by1[RPL], bz0[RPL], bz1[RPL];
@@ -305,8 +334,10 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
         c.fy = static_cast<float>(sizeof(CT) == 4 ? ys[jl] : CT(0));
         c.fz = static_cast<float>(sizeof(CT) == 4 ? zs[jl] : CT(0));
         cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
+        mbar_arrive_remote(&xbar[round & 1], lane);  // release orders the store
       }
     };
+    auto wait_round = [&]() { mbar_wait(&xbar[round & 1], (round >> 1) & 1); };
     auto take = [&](const Cand& w) {
       px = w.x; py = w.y; pz = w.z;
       pfx = w.fx; pfy = w.fy; pfz = w.fz;
@@ -321,7 +352,7 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
     if constexpr (CS > 1) {
       Cand* slot = xbuf + (round & 1) * CS;
       post(slot, hi, lo, j);
-      cg::this_cluster().sync();
+      wait_round();
       uint32_t h = lane < CS ? slot[lane].hi : 0u, l = lane < CS ? slot[lane].lo : 0u;
       uint32_t jj = lane < CS ? slot[lane].j : kNoIndex;
       warp_argmax(h, l, jj);
@@ -350,7 +381,7 @@ __global__ void __launch_bounds__(W * 32) rows_kernel(const SampleParams p) {
       if constexpr (CS > 1) {
         Cand* slot = xbuf + (round & 1) * CS;
         post(slot, jm != kNoIndex ? 1u : 0u, 0u, jm);
-        cg::this_cluster().sync();
+        wait_round();
         uint32_t h = lane < CS ? slot[lane].hi : 0u, l = 0u, jj = lane < CS ? slot[lane].j : kNoIndex;
         warp_argmax(h, l, jj);
         const unsigned who = __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h);
@@ -399,6 +430,7 @@ size_t rows_smem_bytes(int chunk, int W, int CS) {
   bytes += ((np >> 5) + 4 - ((np >> 5) & 3)) * 4;  // sampled bits, 16 B aligned
   bytes += 2 * W * sizeof(uint4);
   bytes += 2 * CS * sizeof(Cand);
+  bytes += 2 * sizeof(uint64_t);  // exchange mbarriers
   return bytes;
 }
 
