@@ -1,0 +1,66 @@
+// Helpers shared by the pruned-row samplers (rows_kernels.cu,
+// morton_kernels.cu): cluster candidate exchange, fp32 box bounds, keys.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "sampler_common.cuh"
+
+namespace pcsk {
+
+namespace rows {
+
+constexpr int kRowsPad = 2;  // zero rows after each chunk (pair processing)
+
+struct Cand {
+  uint32_t hi, lo, j;
+  float fx, fy, fz, pad0, pad1;
+  double x, y, z;
+};
+
+// Cluster exchange without a cluster-wide barrier: each CTA stores its
+// candidate into every CTA's slot and arrives (release, cluster scope) on
+// that CTA's mbarrier for the round; each CTA waits (acquire) on its own.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+               :: "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, int target_rank) {
+  unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(local_bar)), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(target_rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred done;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra WAIT_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
+
+template <bool F2F>
+__device__ __forceinline__ double to_f64(float v) { return F2F ? static_cast<double>(v) : widen_f32(v); }
+template <bool F2F>
+__device__ __forceinline__ double to_f64(double v) { return v; }
+
+__device__ __forceinline__ float f_lo(float v) { return v; }
+__device__ __forceinline__ float f_hi(float v) { return v; }
+__device__ __forceinline__ float f_lo(double v) { return __double2float_rd(v); }
+__device__ __forceinline__ float f_hi(double v) { return __double2float_ru(v); }
+
+// Lower bound (round-down fp32) of the squared distance from the pivot
+// interval [pl, ph] to the box [b0, b1] on one axis.
+__device__ __forceinline__ float gap2(float b0, float b1, float pl, float ph) {
+  const float g = fmaxf(fmaxf(__fsub_rd(b0, ph), __fsub_rd(pl, b1)), 0.0f);
+  return __fmul_rd(g, g);
+}
+
+__device__ __forceinline__ bool key_gt(uint32_t h1, uint32_t l1, uint32_t j1, uint32_t h2,
+                                       uint32_t l2, uint32_t j2) {
+  return h1 > h2 || (h1 == h2 && (l1 > l2 || (l1 == l2 && j1 < j2)));
+}
+
+}  // namespace rows
+
+}  // namespace pcsk

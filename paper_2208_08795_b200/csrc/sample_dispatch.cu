@@ -5,14 +5,29 @@
 
 namespace pcsk {
 
+// Full-window sectors above this size take the Morton-row engine first; the
+// register-resident full kernel wins below it (r01 sweep: cfg5 FPS 2K full
+// 0.43 ms vs Morton 0.73 ms; 4K full 1.70 ms vs Morton 1.50 ms).
+constexpr long long kMortonMin = 3072;
+
 cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
                      std::string* msg) {
   p.nmax = static_cast<int>((nmax_sector + 1) & ~1LL);
   // PCS_SAMPLER=rows forces the pruned-row engine (benchmarking / tests)
   const char* force = std::getenv("PCS_SAMPLER");
   const bool rows = force && std::string(force) == "rows";
+  // full-window sectors: Morton rows beyond the register kernels' sweet
+  // spot (PCS_MORTON=0 selects the storage-order rows, for A/B and tests;
+  // PCS_MORTON_MIN moves the crossover)
+  const char* morton = std::getenv("PCS_MORTON");
+  const bool use_morton = !windowed && !(morton && std::string(morton) == "0");
+  const char* mmin = std::getenv("PCS_MORTON_MIN");
+  const long long morton_min = mmin ? std::atoll(mmin) : kMortonMin;
   cudaError_t e = cudaErrorNotSupported;
-  if (!rows) e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
+  if (use_morton && (rows || nmax_sector > morton_min)) e = run_morton_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && !rows)
+    e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && use_morton) e = run_morton_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported) e = run_rows_any(p, nmax_sector, windowed, st);
   if (e == cudaErrorNotSupported && msg)
     *msg = "sector of " + std::to_string(nmax_sector) +

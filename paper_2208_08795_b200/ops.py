@@ -194,22 +194,31 @@ def quality(xyz: torch.Tensor, idx: torch.Tensor):
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None, dtype: str = "float32") -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
-    the per-sector register kernel for full windows up to 4096 points, the
-    NPDU warp kernel for windows over sectors up to 8192 points, the pruned
-    row engine (one CTA or a cluster) otherwise."""
+    the per-sector register kernel for full windows up to 3072 points, the
+    Morton-row engine for larger full windows (one CTA or a cluster), the
+    TMEM / warp NPDU kernels for windows over sectors up to 8192 points, the
+    storage-order row engine otherwise."""
     import os
 
     sectored = method in ("afps", "npdu_afps")
     nmax = -(-n // (m if sectored else 1))
     windowed = method in ("npdu_fps", "npdu_afps") and k is not None and k < 2 * nmax - 1
-    if (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows":
+    rows = (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows"
+    # Morton capacity: 16 CTAs x (227 KB - 4 KB) / (d + xyz + slot map) bytes per point
+    per_pt = 8 + 3 * (8 if dtype == "float64" else 4) + 4
+    morton_cap = 16 * ((227 * 1024 - 4096) // per_pt // 32 - 2) * 32
+    morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
+              and nmax <= morton_cap)
+    if morton and (rows or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
+        return "morton_rows_kernel"
+    if rows:
         return "rows_kernel"
     if windowed:
         if nmax <= 1024 and (k + 62) // 32 <= 5 and dtype != "float64" and \
                 os.environ.get("PCS_NPDU_TMEM", "1") != "0":
             return "npdu_tmem_kernel"
         return "npdu_warp_kernel" if nmax <= 8192 else "rows_kernel"
-    return "fps_full_kernel" if nmax <= 4096 else "rows_kernel"
+    return "fps_full_kernel"
 
 
 def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,

@@ -123,6 +123,20 @@ def test_distance_trace_bit_exact(pcs, oracle):
         assert (tr[1:] <= tr[:-1]).all()  # monotone (inf - inf would be nan)
 
 
+@pytest.mark.parametrize("morton", ["1", "0"])
+def test_distance_trace_rows_engines(pcs, oracle, monkeypatch, morton):
+    """Trace through the pruned-row engines (the Morton engine writes d[] back
+    through its slot -> index map)."""
+    monkeypatch.setenv("PCS_SAMPLER", "rows")
+    monkeypatch.setenv("PCS_MORTON", morton)
+    pts = synth.random_cloud(700, 405)
+    pts[100:200] = pts[3]
+    idx, _, st, tr = pcs.local_fps(pts, 20, 690, 40, k=None, seed=5, first="random", trace=True)
+    widx, wst, wtr = oracle.local_fps(pts, 20, 690, 40, k=0, first="random", seed=5, trace=True)
+    np.testing.assert_array_equal(idx, widx)
+    np.testing.assert_array_equal(tr, wtr)
+
+
 def test_batched_configs_vs_oracle(oracle):
     import torch
 
@@ -248,17 +262,20 @@ def test_large_sectors_cluster_engine(pcs, oracle):
     _same(got, *want)
 
 
+@pytest.mark.parametrize("morton", ["1", "0"])
 @pytest.mark.parametrize("meth,n,c,m,k", [("fps", 2048, 512, 1, 0), ("afps", 4096, 1024, 4, 0),
                                           ("npdu_afps", 8192, 2048, 16, 65),
                                           ("npdu_fps", 3000, 700, 1, 33), ("afps", 700, 90, 3, 0)])
-def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k):
-    """The pruned-row engine on sizes the other kernels normally take
-    (PCS_SAMPLER=rows), including coincident points and random starts."""
+def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k, morton):
+    """The pruned-row engines (Morton rows and storage-order rows) on sizes the
+    other kernels normally take (PCS_SAMPLER=rows), including coincident
+    points and random starts."""
     import torch
 
     from paper_2208_08795_b200 import sample
 
     monkeypatch.setenv("PCS_SAMPLER", "rows")
+    monkeypatch.setenv("PCS_MORTON", morton)
     xyz = synth.stable_sort_np(synth.uniform_cube(3, n, 5), 0)[0]
     xyz[1, : n // 3] = xyz[1, 0]  # many coincident points
     for first in ("fixed", "random"):
@@ -269,15 +286,16 @@ def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
-@pytest.mark.parametrize("engine", ["auto", "rows"])
+@pytest.mark.parametrize("engine", ["auto", "rows", "slab"])
 def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
     """fp32 subnormals take the exact F2F widening path; +-0 the integer one."""
     import torch
 
     from paper_2208_08795_b200 import sample
 
-    if engine == "rows":
+    if engine != "auto":
         monkeypatch.setenv("PCS_SAMPLER", "rows")
+        monkeypatch.setenv("PCS_MORTON", "0" if engine == "slab" else "1")
     xyz = synth.uniform_cube(2, 3000, 8) * np.float32(1e-36)
     xyz[0, ::5, 0] = np.float32(3e-41)   # subnormal
     xyz[0, 1::5, 1] = np.float32(-0.0)
@@ -286,6 +304,38 @@ def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
         idx, st = sample(torch.from_numpy(xyz).cuda(), 600, method=meth, m=m, k=k or None)
         want_idx, want_st = oracle.sample_batch_f32(meth, xyz, 600, m, k)
         np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=meth)
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
+@pytest.mark.parametrize("cloud", ["cube", "primitives", "dupes", "f64"])
+def test_morton_rows_large_sectors(pcs, oracle, cloud):
+    """Full-window sectors past 4096 points take the Morton-row engine (CTA
+    Morton sort, orig-index row keys): one CTA at 8K, clusters of 2/4/8 at
+    16K/32K/60K; clustered, duplicated and fp64 inputs; random starts."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    for n, c, m in ((8192, 2048, 1), (16384, 1500, 1), (32768, 700, 1), (60000, 300, 1),
+                    (40000, 4000, 4)):
+        if cloud == "primitives":
+            xyz = synth.primitives(1, n, 6, seed=n)
+        else:
+            xyz = synth.uniform_cube(1, n, n + 1)
+        if cloud == "dupes":
+            xyz[0, 1::3] = xyz[0, 0]
+            xyz[0, 2::7] = xyz[0, 5]
+        if cloud == "f64":
+            pts = synth.random_cloud(n, n)
+            got = pcs.afps(pts, c, m, seed=n) if m > 1 else pcs.fps(pts, c, seed=n)
+            want = oracle.sample("afps" if m > 1 else "fps", pts, c, m, first="random", seed=n)
+            _same(got, *want)
+            continue
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="afps" if m > 1 else "fps",
+                         m=m, first="random", seed=n)
+        want_idx, want_st = oracle.sample_batch_f32("afps" if m > 1 else "fps", xyz, c, m, 0,
+                                                    "random", n)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{cloud} {n}")
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
