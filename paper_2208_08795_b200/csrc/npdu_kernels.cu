@@ -458,12 +458,19 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     const long long index_off = g.begin + p.index_base;
     int* out32 = static_cast<int*>(p.out_idx) + out_base;
     long long* out64 = static_cast<long long*>(p.out_idx) + out_base;
-    if (lane == 0) {
-      if (p.idx64) out64[0] = index_off + cur;
-      else out32[0] = static_cast<int>(index_off + cur);
-      sampled[cur >> 5] |= 1u << (cur & 31);
-    }
-    __syncwarp();
+    const bool idx64 = p.idx64 != 0;
+    double* const trace = p.trace;
+    // output indices are buffered one per lane (sample t in lane t % 32) and
+    // stored 32 at a time; the sampled bitmap is only needed by the
+    // all-zero slow path, which folds the outputs into it on demand
+    int ob = cur;
+    auto flush = [&](int t0, int cnt) {
+      if (lane < cnt) {
+        if (idx64) out64[t0 + lane] = index_off + ob;
+        else out32[t0 + lane] = static_cast<int>(index_off + ob);
+      }
+    };
+    int marked = 0;  // outputs [0, marked) are in the bitmap
     const long long K = p.K;
     const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
     unsigned writes = 0;
@@ -503,7 +510,7 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
           rm_j = jj;
         }
       }
-      if (p.trace) {
+      if (trace) {
         tm_wait_st();
         for (int r = 0; r < rows; ++r) {
           uint32_t t[2];
@@ -511,13 +518,26 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
           tm_wait_ld();
           const int j = (r << 5) + lane;
           if (j < n)
-            p.trace[static_cast<long long>(it - 1) * n + j] =
+            trace[static_cast<long long>(it - 1) * n + j] =
                 __hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0]));
         }
       }
       uint32_t hi = rm_hi, lo = rm_lo, j = rm_j;
       warp_argmax(hi, lo, j);
       if ((hi | lo) == 0u) {
+        // fold outputs [marked, it) into the bitmap: whole blocks from
+        // global memory, the current block from the lanes' buffers
+        const int t_blk = (it - 1) & ~31;
+        __syncwarp();
+        for (int t = marked + lane; t < t_blk; t += 32) {
+          const long long v = idx64 ? out64[t] : static_cast<long long>(out32[t]);
+          const int jl = static_cast<int>(v - index_off);
+          atomicOr(&sampled[jl >> 5], 1u << (jl & 31));
+        }
+        if (lane <= ((it - 1) & 31) && t_blk + lane >= marked)
+          atomicOr(&sampled[ob >> 5], 1u << (ob & 31));
+        marked = it;
+        __syncwarp();
         uint32_t jm = kNoIndex;
         for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
           const unsigned free_bits = ~sampled[w];
@@ -529,13 +549,10 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
         j = __reduce_min_sync(kFull, jm);
       }
       cur = static_cast<int>(j);
-      if (lane == 0) {
-        if (p.idx64) out64[it] = index_off + cur;
-        else out32[it] = static_cast<int>(index_off + cur);
-        sampled[cur >> 5] |= 1u << (cur & 31);
-      }
-      __syncwarp();
+      if (lane == (it & 31)) ob = cur;
+      if ((it & 31) == 31) flush(it - 31, 32);
     }
+    if (((g.quota - 1) & 31) != 31) flush((g.quota - 1) & ~31, ((g.quota - 1) & 31) + 1);
     tm_wait_st();
     const unsigned ws = __reduce_add_sync(kFull, writes);
     if (p.stats && lane == 0) {

@@ -339,6 +339,29 @@ def test_morton_rows_large_sectors(pcs, oracle, cloud):
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("index_dtype", ["int32", "int64"])
+def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
+    """fp32 NPDU sectors <= 1024 points (the TMEM kernel): heavily duplicated
+    clouds drive the all-zero slow path (lowest unsampled index) many times;
+    quotas that are not multiples of 32 exercise the buffered output flush."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    rng = np.random.default_rng(9)
+    for n, c, m, k in ((4096, 1232, 4, 129), (3000, 2995, 3, 65), (1024, 77, 1, 33),
+                       (2048, 2048, 2, 97)):
+        xyz = synth.uniform_cube(3, n, n)
+        xyz[0] = xyz[0][rng.integers(0, 40, n)]            # 40 distinct points
+        xyz[1, : n // 2] = xyz[1, 7]                        # half coincident
+        for first in ("fixed", "random"):
+            idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="npdu_afps", m=m, k=k,
+                             first=first, seed=n, index_dtype=getattr(torch, index_dtype))
+            want_idx, want_st = oracle.sample_batch_f32("npdu_afps", xyz, c, m, k, first, n)
+            np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{n} {first}")
+            np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
