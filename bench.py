@@ -333,8 +333,20 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item()) / args.steps
         r = e2e_step()
+        # the PCIe floor on this box: one plain H2D of the same pinned batch
+        dst = torch.empty(pinned.shape, dtype=pinned.dtype, device=dev)
+        h2d = []
+        for _ in range(5):
+            es.record()
+            dst.copy_(pinned, non_blocking=True)
+            ee.record()
+            torch.cuda.synchronize()
+            h2d.append(es.elapsed_time(ee))
+        del dst
         e2e = {"value": world * B * C / (e_ms * 1e-3), "unit": "sampled points/s",
-               "ms_per_step": e_ms, "h2d_bytes_per_step": int(pinned.numel() * 4),
+               "ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
+               "h2d_gbps": pinned.numel() * pinned.element_size() / min(h2d) / 1e6,
+               "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
                "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in r)),
                "path": "pcs.sample(pinned host tensor): chunked H2D overlapped with sort+sample, "
                        "D2H of indices, stats (and perm when sorting)"}

@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
                    is_subnormal_f32(static_cast<float>(ys[i])) ||
                    is_subnormal_f32(static_cast<float>(zs[i]));
   if (CS > 1 && threadIdx.x == 0) {
-    mbar_init(&xbar[0], CS);
-    mbar_init(&xbar[1], CS);
+    mbar_init(&xbar[0], 1);  // one local arrive.expect_tx per round
+    mbar_init(&xbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const bool any_sub = __syncthreads_or(sub_local) != 0;
@@ -354,23 +354,36 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
     }
     MPROF_T(t3);
     bool zero = (hi | lo) == 0u;
+    // every CTA sends (key, index, pivot coordinates) to slot [rank] of
+    // every CTA with st.async; 24 B (fp32 coordinates) or 40 B (fp64)
+    constexpr unsigned kMsg = sizeof(CT) == 4 ? 24u : 40u;
     auto post = [&](Cand* slot, uint32_t h, uint32_t l, uint32_t jj, uint32_t at) {
       if (warp == 0 && lane < CS) {
-        Cand c;
-        c.hi = h; c.lo = l; c.j = jj; c.pad0 = c.pad1 = 0.f;
         const int i = jj == kNoIndex ? 0 : static_cast<int>(at);
-        c.x = to_f64<F2F>(xs[i]); c.y = to_f64<F2F>(ys[i]); c.z = to_f64<F2F>(zs[i]);
-        c.fx = static_cast<float>(sizeof(CT) == 4 ? xs[i] : CT(0));
-        c.fy = static_cast<float>(sizeof(CT) == 4 ? ys[i] : CT(0));
-        c.fz = static_cast<float>(sizeof(CT) == 4 ? zs[i] : CT(0));
-        cg::this_cluster().map_shared_rank(slot, lane)[rank] = c;
-        mbar_arrive_remote(&xbar[round & 1], lane);
+        const uint32_t rs = mapa(slot + rank, lane), rb = mapa(&xbar[round & 1], lane);
+        if constexpr (sizeof(CT) == 4) {
+          st_async_v4(rs, rb, h, l, jj, __float_as_uint(static_cast<float>(xs[i])));
+          st_async_v2(rs + 16, rb, __float_as_uint(static_cast<float>(ys[i])),
+                      __float_as_uint(static_cast<float>(zs[i])));
+        } else {
+          const double x = static_cast<double>(xs[i]), y = static_cast<double>(ys[i]),
+                       z = static_cast<double>(zs[i]);
+          st_async_v4(rs, rb, h, l, jj, 0u);
+          st_async_v4(rs + 32, rb, __double2loint(x), __double2hiint(x), __double2loint(y),
+                      __double2hiint(y));
+          st_async_v2(rs + 48, rb, __double2loint(z), __double2hiint(z));
+        }
       }
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[round & 1], CS * kMsg);
     };
     auto wait_round = [&]() { mbar_wait(&xbar[round & 1], (round >> 1) & 1); };
     auto take = [&](const Cand& w) {
-      px = w.x; py = w.y; pz = w.z;
-      pfx = w.fx; pfy = w.fy; pfz = w.fz;
+      if constexpr (sizeof(CT) == 4) {
+        pfx = w.fx; pfy = w.fy; pfz = w.fz;
+        px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
+      } else {
+        px = w.x; py = w.y; pz = w.z;
+      }
     };
     auto take_local = [&](uint32_t i) {
       px = to_f64<F2F>(xs[i]); py = to_f64<F2F>(ys[i]); pz = to_f64<F2F>(zs[i]);

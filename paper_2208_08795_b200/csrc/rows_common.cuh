@@ -12,10 +12,10 @@ namespace rows {
 
 constexpr int kRowsPad = 2;  // zero rows after each chunk (pair processing)
 
-struct Cand {
+struct alignas(16) Cand {  // 64 B: st.async writes 16 B-aligned pieces
   uint32_t hi, lo, j;
   float fx, fy, fz, pad0, pad1;
-  double x, y, z;
+  double x, y, z, pad2;
 };
 
 // Cluster exchange without a cluster-wide barrier: each CTA stores its
@@ -29,6 +29,28 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, int targ
   unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(local_bar)), remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(target_rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
+}
+// Asynchronous DSMEM stores that complete-tx on the receiver's mbarrier
+// (no release fence on the sender); the receiver arms the round with one
+// local arrive.expect_tx for the bytes all senders will deliver.
+__device__ __forceinline__ uint32_t mapa(const void* local, int target_rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(remote) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(local))), "r"(target_rank));
+  return remote;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t rbar, uint32_t a, uint32_t b,
+                                            uint32_t c, uint32_t d) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               :: "r"(raddr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t rbar, uint32_t a, uint32_t b) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+               :: "r"(raddr), "r"(a), "r"(b), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
