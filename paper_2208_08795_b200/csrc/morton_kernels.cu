@@ -54,6 +54,14 @@ __device__ __forceinline__ int f2ord(float f) {
 }
 __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
+// One warp's candidate as seen by every CTA of the cluster: key, sector-local
+// index, slot in the sender CTA, pivot coordinates (3 floats or 3 doubles).
+struct alignas(16) Msg {
+  uint32_t hi, lo, j, pos;
+  uint32_t c[6];
+  uint32_t pad[2];
+};
+
 }  // namespace
 
 // Local slot layout: the CTA's storage points (sector rows R % CS == rank,
@@ -79,8 +87,8 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
   uint32_t* orig = reinterpret_cast<uint32_t*>(zs + np);
   unsigned* sampled = orig + np;
   uint4* cand = reinterpret_cast<uint4*>(sampled + (np >> 5) + 4 - ((np >> 5) & 3));
-  Cand* xbuf = reinterpret_cast<Cand*>(cand + 2 * W);            // [2][CS]
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + 2 * CS);    // [2]
+  Msg* xbuf = reinterpret_cast<Msg*>(cand + 2 * W);              // [2][CS * W]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + (CS > 1 ? 2 * CS * W : 0));  // [2]
   int* scratch = reinterpret_cast<int*>(xbar + 2);                // [8]
   if (sizeof(CT) < sizeof(double) && p.f64) __trap();
   auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
@@ -342,49 +350,6 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
       j = j == kNoIndex ? kNoIndex : j >> 5;
     }
     MPROF_T(t2);
-    if constexpr (W > 1) {
-      uint4* buf = cand + (round & 1) * W;
-      if (lane == 0) buf[warp] = make_uint4(hi, lo, j, pos);
-      __syncthreads();
-      const uint4 v = lane < W ? buf[lane] : make_uint4(0, 0, kNoIndex, 0);
-      hi = v.x; lo = v.y; j = v.z;
-      warp_argmax(hi, lo, j);
-      const unsigned who = __ballot_sync(kFull, lane < W && v.x == hi && v.y == lo && v.z == j);
-      pos = buf[who ? __ffs(who) - 1 : 0].w;
-    }
-    MPROF_T(t3);
-    bool zero = (hi | lo) == 0u;
-    // every CTA sends (key, index, pivot coordinates) to slot [rank] of
-    // every CTA with st.async; 24 B (fp32 coordinates) or 40 B (fp64)
-    constexpr unsigned kMsg = sizeof(CT) == 4 ? 24u : 40u;
-    auto post = [&](Cand* slot, uint32_t h, uint32_t l, uint32_t jj, uint32_t at) {
-      if (warp == 0 && lane < CS) {
-        const int i = jj == kNoIndex ? 0 : static_cast<int>(at);
-        const uint32_t rs = mapa(slot + rank, lane), rb = mapa(&xbar[round & 1], lane);
-        if constexpr (sizeof(CT) == 4) {
-          st_async_v4(rs, rb, h, l, jj, __float_as_uint(static_cast<float>(xs[i])));
-          st_async_v2(rs + 16, rb, __float_as_uint(static_cast<float>(ys[i])),
-                      __float_as_uint(static_cast<float>(zs[i])));
-        } else {
-          const double x = static_cast<double>(xs[i]), y = static_cast<double>(ys[i]),
-                       z = static_cast<double>(zs[i]);
-          st_async_v4(rs, rb, h, l, jj, 0u);
-          st_async_v4(rs + 32, rb, __double2loint(x), __double2hiint(x), __double2loint(y),
-                      __double2hiint(y));
-          st_async_v2(rs + 48, rb, __double2loint(z), __double2hiint(z));
-        }
-      }
-      if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[round & 1], CS * kMsg);
-    };
-    auto wait_round = [&]() { mbar_wait(&xbar[round & 1], (round >> 1) & 1); };
-    auto take = [&](const Cand& w) {
-      if constexpr (sizeof(CT) == 4) {
-        pfx = w.fx; pfy = w.fy; pfz = w.fz;
-        px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
-      } else {
-        px = w.x; py = w.y; pz = w.z;
-      }
-    };
     auto take_local = [&](uint32_t i) {
       px = to_f64<F2F>(xs[i]); py = to_f64<F2F>(ys[i]); pz = to_f64<F2F>(zs[i]);
       if constexpr (sizeof(CT) == 4) {
@@ -392,28 +357,80 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
         pfz = static_cast<float>(zs[i]);
       }
     };
+    // CS > 1: every warp sends its candidate straight to every CTA of the
+    // cluster (st.async + complete_tx on the receiver's mbarrier); each CTA
+    // reduces the W x CS candidates itself -- no CTA barrier on the way
+    constexpr unsigned kMsg = sizeof(CT) == 4 ? 32u : 40u;
+    auto exchange = [&](uint32_t h, uint32_t l, uint32_t jj, uint32_t at, bool& mine_out) {
+      Msg* mb = xbuf + (round & 1) * (CS * W);
+      if (lane < CS) {
+        const int i = jj == kNoIndex ? 0 : static_cast<int>(at);
+        const uint32_t rs = mapa(mb + rank * W + warp, lane), rb = mapa(&xbar[round & 1], lane);
+        st_async_v4(rs, rb, h, l, jj, at);
+        if constexpr (sizeof(CT) == 4) {
+          st_async_v4(rs + 16, rb, __float_as_uint(static_cast<float>(xs[i])),
+                      __float_as_uint(static_cast<float>(ys[i])),
+                      __float_as_uint(static_cast<float>(zs[i])), 0u);
+        } else {
+          const double x = static_cast<double>(xs[i]), y = static_cast<double>(ys[i]),
+                       z = static_cast<double>(zs[i]);
+          st_async_v4(rs + 16, rb, __double2loint(x), __double2hiint(x), __double2loint(y),
+                      __double2hiint(y));
+          st_async_v2(rs + 32, rb, __double2loint(z), __double2hiint(z));
+        }
+      }
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[round & 1], CS * W * kMsg);
+      mbar_wait(&xbar[round & 1], (round >> 1) & 1);
+      uint32_t bh = 0u, bl = 0u, bj = kNoIndex;
+      int be = 0;
+#pragma unroll
+      for (int e0 = 0; e0 < CS * W; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < CS * W) {
+          const uint4 k = *reinterpret_cast<const uint4*>(mb + e);
+          if (key_gt(k.x, k.y, k.z, bh, bl, bj)) { bh = k.x; bl = k.y; bj = k.z; be = e; }
+        }
+      }
+      uint32_t h2 = bh, l2 = bl, j2 = bj;
+      warp_argmax(h2, l2, j2);
+      const unsigned who = __ballot_sync(kFull, bh == h2 && bl == l2 && bj == j2);
+      const int e = __shfl_sync(kFull, be, __ffs(who) - 1);
+      const Msg& w = mb[e];
+      if ((h2 | l2) != 0u || j2 != kNoIndex) {
+        if constexpr (sizeof(CT) == 4) {
+          pfx = __uint_as_float(w.c[0]); pfy = __uint_as_float(w.c[1]); pfz = __uint_as_float(w.c[2]);
+          px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
+        } else {
+          px = __hiloint2double(static_cast<int>(w.c[1]), static_cast<int>(w.c[0]));
+          py = __hiloint2double(static_cast<int>(w.c[3]), static_cast<int>(w.c[2]));
+          pz = __hiloint2double(static_cast<int>(w.c[5]), static_cast<int>(w.c[4]));
+        }
+      }
+      mine_out = e / W == rank;
+      pos = w.pos;
+      hi = h2; lo = l2; j = j2;
+      ++round;
+    };
     // mine: this CTA holds the winner at slot `pos`
     bool mine = true;
     if constexpr (CS > 1) {
-      Cand* slot = xbuf + (round & 1) * CS;
-      post(slot, hi, lo, j, pos);
-      wait_round();
-      uint32_t h = lane < CS ? slot[lane].hi : 0u, l = lane < CS ? slot[lane].lo : 0u;
-      uint32_t jj = lane < CS ? slot[lane].j : kNoIndex;
-      warp_argmax(h, l, jj);
-      zero = (h | l) == 0u;
-      mine = !zero && h == hi && l == lo && jj == j;
-      hi = h; lo = l; j = jj;
-      if (!zero) {
-        const unsigned who =
-            __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h && slot[lane].lo == l);
-        take(slot[__ffs(who) - 1]);
-      }
+      exchange(hi, lo, j, pos, mine);
     } else {
-      if (!zero) take_local(pos);
+      if constexpr (W > 1) {
+        uint4* buf = cand + (round & 1) * W;
+        if (lane == 0) buf[warp] = make_uint4(hi, lo, j, pos);
+        __syncthreads();
+        const uint4 v = lane < W ? buf[lane] : make_uint4(0, 0, kNoIndex, 0);
+        hi = v.x; lo = v.y; j = v.z;
+        warp_argmax(hi, lo, j);
+        const unsigned who = __ballot_sync(kFull, lane < W && v.x == hi && v.y == lo && v.z == j);
+        pos = buf[who ? __ffs(who) - 1 : 0].w;
+        ++round;
+      }
+      if ((hi | lo) != 0u) take_local(pos);
     }
-    ++round;
-    if (zero) {
+    MPROF_T(t3);
+    if ((hi | lo) == 0u) {
       // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
       uint32_t jm = kNoIndex;
       for (int i = lane; i < held; i += 32)
@@ -427,21 +444,13 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
           if (hit) { at = static_cast<uint32_t>(i0 + __ffs(hit) - 1); break; }
         }
       if constexpr (CS > 1) {
-        Cand* slot = xbuf + (round & 1) * CS;
-        post(slot, jm != kNoIndex ? 1u : 0u, 0u, jm, at);
-        wait_round();
-        uint32_t h = lane < CS ? slot[lane].hi : 0u, l = 0u, jj = lane < CS ? slot[lane].j : kNoIndex;
-        warp_argmax(h, l, jj);
-        const unsigned who = __ballot_sync(kFull, lane < CS && slot[lane].j == jj && slot[lane].hi == h);
-        take(slot[__ffs(who) - 1]);
-        mine = jj == jm && jm != kNoIndex;
-        j = jj;
-        ++round;
+        // every warp of the CTA posts the same (1, 0, jm) candidate
+        exchange(jm != kNoIndex ? 1u : 0u, 0u, jm, at, mine);
       } else {
         j = jm;
+        pos = at;
         take_local(at);
       }
-      pos = at;
     }
     cur = static_cast<int>(j);
     if (rank == 0 && threadIdx.x == 0) {
@@ -482,7 +491,7 @@ size_t morton_smem_bytes(int np, int W, int CS) {
   size_t bytes = static_cast<size_t>(np) * (8 + 3 * sizeof(CT) + 4);
   bytes += ((np >> 5) + 4 - ((np >> 5) & 3)) * 4;
   bytes += 2 * W * sizeof(uint4);
-  bytes += 2 * CS * sizeof(Cand);
+  bytes += CS > 1 ? 2 * CS * W * sizeof(Msg) : 0;
   bytes += 2 * sizeof(uint64_t) + 8 * sizeof(int);
   return bytes;
 }
@@ -521,12 +530,17 @@ cudaError_t launch_morton(SampleParams p, int np, cudaStream_t st) {
 // fewer rows to update per iteration than slab rows, so the fixed per-warp
 // reduction cost argues for the smallest W that holds the rows
 // (PCS_MORTON_W overrides for tuning).
+int morton_w(int rows) {
+  int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
+  if (const char* e = std::getenv("PCS_MORTON_W")) w = std::max(w, std::atoi(e));
+  return w > 16 ? 32 : w;
+}
+
 template <typename CT, int CS>
 cudaError_t launch_morton_w(SampleParams p, int chunk, cudaStream_t st) {
   const int rows = (chunk + 31) / 32;
   const int np = (rows + kRowsPad) * 32;
-  int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
-  if (const char* e = std::getenv("PCS_MORTON_W")) w = std::max(w, std::atoi(e));
+  const int w = morton_w(rows);
   if (rows > 32 * w) return cudaErrorNotSupported;
   switch (w) {
     case 4: return launch_morton<CT, 4, CS>(p, np, st);
@@ -536,22 +550,26 @@ cudaError_t launch_morton_w(SampleParams p, int chunk, cudaStream_t st) {
   }
 }
 
+// Smallest cluster whose per-CTA share (rows interleaved over the CTAs)
+// fits shared memory with its exchange buffers.
 template <typename CT>
 cudaError_t launch_morton_cs(SampleParams p, long long n, cudaStream_t st) {
-  const int cap = static_cast<int>(((kMaxSmem - 4096) / (12 + 3 * sizeof(CT)) / 32 - kRowsPad) * 32);
-  const long long cs_needed = (n + cap - 1) / cap;
-  int CS = 1;
-  while (CS < cs_needed) CS *= 2;
-  if (CS > 16) return cudaErrorNotSupported;
   const long long srows = (n + 31) / 32;
-  const int chunk = static_cast<int>((srows + CS - 1) / CS * 32);
-  switch (CS) {
-    case 1: return launch_morton_w<CT, 1>(p, chunk, st);
-    case 2: return launch_morton_w<CT, 2>(p, chunk, st);
-    case 4: return launch_morton_w<CT, 4>(p, chunk, st);
-    case 8: return launch_morton_w<CT, 8>(p, chunk, st);
-    default: return launch_morton_w<CT, 16>(p, chunk, st);
+  for (int CS = 1; CS <= 16; CS *= 2) {
+    const int rows = static_cast<int>((srows + CS - 1) / CS);
+    const int w = morton_w(rows);
+    if (rows > 32 * w) continue;
+    if (morton_smem_bytes<CT>((rows + kRowsPad) * 32, w, CS) > kMaxSmem) continue;
+    const int chunk = rows * 32;
+    switch (CS) {
+      case 1: return launch_morton_w<CT, 1>(p, chunk, st);
+      case 2: return launch_morton_w<CT, 2>(p, chunk, st);
+      case 4: return launch_morton_w<CT, 4>(p, chunk, st);
+      case 8: return launch_morton_w<CT, 8>(p, chunk, st);
+      default: return launch_morton_w<CT, 16>(p, chunk, st);
+    }
   }
+  return cudaErrorNotSupported;
 }
 
 cudaError_t run_morton_any(SampleParams p, long long n, cudaStream_t st) {

@@ -191,6 +191,25 @@ def quality(xyz: torch.Tensor, idx: torch.Tensor):
     return cov, sep
 
 
+def _morton_fits(n: int, dtype: str) -> bool:
+    """Mirror of launch_morton_cs (csrc/morton_kernels.cu): some cluster size
+    <= 16 whose per-CTA rows fit shared memory with the exchange buffers."""
+    ct = 8 if dtype == "float64" else 4
+    srows = -(-n // 32)
+    for cs in (1, 2, 4, 8, 16):
+        rows = -(-srows // cs)
+        w = 4 if rows <= 128 else 8 if rows <= 256 else 16
+        if rows > 32 * w:
+            continue
+        np_ = (rows + 2) * 32
+        nbytes = np_ * (8 + 3 * ct + 4) + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
+        nbytes += 2 * cs * w * 48 if cs > 1 else 0
+        nbytes += 2 * 8 + 8 * 4
+        if nbytes <= 227 * 1024:
+            return True
+    return False
+
+
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None, dtype: str = "float32") -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
@@ -204,11 +223,8 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     nmax = -(-n // (m if sectored else 1))
     windowed = method in ("npdu_fps", "npdu_afps") and k is not None and k < 2 * nmax - 1
     rows = (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows"
-    # Morton capacity: 16 CTAs x (227 KB - 4 KB) / (d + xyz + slot map) bytes per point
-    per_pt = 8 + 3 * (8 if dtype == "float64" else 4) + 4
-    morton_cap = 16 * ((227 * 1024 - 4096) // per_pt // 32 - 2) * 32
     morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
-              and nmax <= morton_cap)
+              and _morton_fits(nmax, dtype))
     if morton and (rows or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
         return "morton_rows_kernel"
     if rows:
