@@ -1,4 +1,6 @@
 // Full-window FPS / AFPS kernels (see sampler_common.cuh for the layout).
+#include <cstdlib>
+
 #include "sampler_common.cuh"
 
 namespace pcsk {
@@ -25,9 +27,11 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
     const bool valid = j < n;
     vmask |= valid ? (1u << k) : 0u;
     if constexpr (REGC) {
-      x[k] = valid ? gs.xs[j] : 0.0;
-      y[k] = valid ? gs.ys[j] : 0.0;
-      z[k] = valid ? gs.zs[j] : 0.0;
+      // padding slots: NaN coordinates make every `dist <= d` false there
+      const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+      x[k] = valid ? gs.xs[j] : kNaN;
+      y[k] = valid ? gs.ys[j] : kNaN;
+      z[k] = valid ? gs.zs[j] : kNaN;
     }
     d[k] = valid ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
   }
@@ -43,9 +47,9 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
     unsigned long long best = 0;
     int bs = -1;
     // Branch-free over the slots so independent slots interleave (ILP).
-    // Padding slots (j >= n) hold d = 0 and finite coordinates: they never
-    // win the argmax (best starts at 0 with a strict >) and their writes are
-    // masked out of the count.
+    // Padding slots (j >= n) hold d = 0 and NaN coordinates (REGC): they
+    // never win the argmax (best starts at 0 with a strict >) and never
+    // write (NaN compares false).
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       const int j = k * T + t;
@@ -54,7 +58,7 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
       const double zz = REGC ? z[REGC ? k : 0] : gs.zs[min(j, n - 1)];
       const double dist = dist2(xx, yy, zz, px, py, pz);
       const bool lower = dist <= d[k];
-      writes += (lower && ((vmask >> k) & 1u)) ? 1u : 0u;
+      writes += (lower && (REGC || ((vmask >> k) & 1u))) ? 1u : 0u;
       d[k] = lower ? dist : d[k];
       const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
       if (bits > best) {
@@ -118,6 +122,21 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   if (n <= 64) return run_full<2, 1, true>(p, st);
   if (n <= 128) return run_full<4, 1, true>(p, st);
   if (n <= 256) return run_full<8, 1, true>(p, st);
+  // 8 slots per thread (twice the warps, ~120 registers) hides more latency
+  // when an SM holds one sector or at least four; with ~2 sectors per SM the
+  // 16-slot form measured faster (r01 sweep: cfg5 FPS 2K 0.374 vs 0.400 ms;
+  // AFPS M=4 at 8K 1.69 vs 1.33 ms, cfg1 0.283 vs 0.262 ms). PCS_FULL_P
+  // (8 or 16) overrides.
+  const long long sectors = p.B * p.M;
+  bool p8 = sectors >= 4 * 148 || sectors <= 148;
+  if (const char* pe = std::getenv("PCS_FULL_P")) p8 = std::atoi(pe) == 8;
+  if (p8) {
+    if (n <= 512) return run_full<8, 2, true>(p, st);
+    if (n <= 1024) return run_full<8, 4, true>(p, st);
+    if (n <= 2048) return run_full<8, 8, true>(p, st);
+    if (n <= 4096) return run_full<8, 16, true>(p, st);
+    return cudaErrorNotSupported;
+  }
   if (n <= 512) return run_full<16, 1, true>(p, st);
   if (n <= 1024) return run_full<16, 2, true>(p, st);
   if (n <= 2048) return run_full<16, 4, true>(p, st);
