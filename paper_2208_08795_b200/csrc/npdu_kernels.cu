@@ -393,17 +393,24 @@ __device__ __forceinline__ void tm_store_rows(uint32_t a, const double (&v)[RMAX
   }
 }
 
-__host__ __device__ __forceinline__ int tm_cols_per_warp(int nmax, int rmax) {
-  return 2 * (((nmax + 31) >> 5) + rmax);
+// Per-warp capacity NCAP points (a compile-time stride: xs/ys/zs at fixed
+// offsets, so one address serves all three loads). The window's RMAX rows
+// are clamped into [0, max(NCAP/32, RMAX)) rows, so no padding rows are read
+// or written beyond that.
+__host__ __device__ constexpr int tm_rows_alloc(int ncap, int rmax) {
+  return (ncap >> 5) > rmax ? (ncap >> 5) : rmax;
+}
+__host__ __device__ constexpr int tm_cols_per_warp(int ncap, int rmax) {
+  return 2 * tm_rows_alloc(ncap, rmax);
+}
+__host__ __device__ constexpr size_t tm_warp_smem(int ncap) {
+  return (size_t(12) * ncap + 4 * ((ncap >> 5) + 8) + 15) & ~size_t(15);
 }
 
-__host__ __device__ __forceinline__ size_t tm_warp_smem(int nmax) {
-  return (size_t(12) * nmax + 4 * ((nmax + 31) / 32 + 8) + 15) & ~size_t(15);
-}
-
-// fp32 input, sectors <= 1024 points (one row maximum per lane)
-template <int RMAX>
+// fp32 input, sectors <= NCAP <= 1024 points (one row maximum per lane)
+template <int RMAX, int NCAP>
 __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
+  static_assert(NCAP >= 32 * RMAX && NCAP <= 1024, "capacity");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tm_base_sh;
   const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -421,22 +428,23 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     const long long b = flat / p.M, s = flat % p.M;
     const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
     const int n = g.n;
-    const int cpw = tm_cols_per_warp(p.nmax, RMAX);
+    constexpr int cpw = tm_cols_per_warp(NCAP, RMAX);
     // this warp's TMEM: lane quarter (gid % 4), column block (gid / 4)
     const uint32_t tm = tm_base + ((static_cast<uint32_t>(gid & 3) * 32u) << 16) +
                         static_cast<uint32_t>((gid >> 2) * cpw);
-    unsigned char* base = smem + static_cast<size_t>(gid) * tm_warp_smem(p.nmax);
+    unsigned char* base = smem + static_cast<size_t>(gid) * tm_warp_smem(NCAP);
     float* xs = reinterpret_cast<float*>(base);
-    float* ys = xs + p.nmax;
-    float* zs = ys + p.nmax;
-    unsigned* sampled = reinterpret_cast<unsigned*>(zs + p.nmax);
+    float* ys = xs + NCAP;
+    float* zs = ys + NCAP;
+    unsigned* sampled = reinterpret_cast<unsigned*>(zs + NCAP);
     stage_sector(static_cast<const float*>(p.xyz) + (b * p.N + g.begin) * 3, n, xs, ys, zs, lane, 32);
     const int rows = (n + 31) >> 5;
     for (int w = lane; w < rows + 8; w += 32) sampled[w] = 0u;
     // d = +inf on the sector, 0 on the pad rows
     {
       const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-      for (int r = 0; r < rows + RMAX; ++r) {
+#pragma unroll 1
+      for (int r = 0; r < tm_rows_alloc(NCAP, RMAX); ++r) {
         const int j = (r << 5) + lane;
         const double v = j < n ? kInf : 0.0;
         uint32_t t[2] = {static_cast<uint32_t>(__double2loint(v)), static_cast<uint32_t>(__double2hiint(v))};
@@ -481,14 +489,18 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       const int wb = cur >= half_down ? cur - half_down : 0;
       const int we = min(n, cur + half_up);
       evals += static_cast<unsigned long long>(we - wb);
-      const int r_lo = wb >> 5;
+      // the RMAX rows from r_lo cover the window; near the sector's end
+      // they are shifted down so they stay inside the allocated rows (the
+      // extra rows are masked out and stored back unchanged)
+      const int r_lo = min(wb >> 5, max(rows - RMAX, 0));
       const int j0 = (r_lo << 5) + lane;
       double dj[RMAX], dist[RMAX];
       tm_wait_st();
       tm_load_rows<RMAX>(tm + 2 * r_lo, dj);
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
-        const int jc = min(j0 + 32 * q, n - 1);
+        // slots past n hold stale shared memory: evaluated, never used
+        const int jc = j0 + 32 * q;
         dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
                         static_cast<double>(zs[jc]), px, py, pz);
       }
@@ -570,10 +582,10 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tm_base), "r"(tm_cols));
 }
 
-template <int RMAX>
+template <int RMAX, int NCAP>
 cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
-  const int cpw = tm_cols_per_warp(p.nmax, RMAX);
-  const size_t wsm = tm_warp_smem(p.nmax);
+  constexpr int cpw = tm_cols_per_warp(NCAP, RMAX);
+  constexpr size_t wsm = tm_warp_smem(NCAP);
   const long long sectors = p.B * p.M;
   // warps per CTA (one CTA per SM): TMEM holds 4 lane quarters x (512 / cpw)
   // column blocks; shared memory and 32 warps bound it too
@@ -585,7 +597,7 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
   const size_t smem = wsm * G;
-  auto kern = npdu_tmem_kernel<RMAX>;
+  auto kern = npdu_tmem_kernel<RMAX, NCAP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -600,9 +612,15 @@ cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
   const bool use_tmem = !(tmv && tmv[0] == '0');
   const long long rows_needed = (p.K + 62) / 32;
   if (use_tmem && !p.f64 && n <= 1024 && rows_needed <= 5) {
-    if (rows_needed <= 2) return run_npdu_tmem<2>(p, st);
-    if (rows_needed <= 3) return run_npdu_tmem<3>(p, st);
-    return run_npdu_tmem<5>(p, st);
+    auto by_cap = [&](auto rmax_tag) {
+      constexpr int R = decltype(rmax_tag)::value;
+      if (n <= 256) return run_npdu_tmem<R, 256>(p, st);
+      if (n <= 512) return run_npdu_tmem<R, 512>(p, st);
+      return run_npdu_tmem<R, 1024>(p, st);
+    };
+    if (rows_needed <= 2) return by_cap(std::integral_constant<int, 2>{});
+    if (rows_needed <= 3) return by_cap(std::integral_constant<int, 3>{});
+    return by_cap(std::integral_constant<int, 5>{});
   }
   if (n <= 1024) return run_npdu_rpl<1>(p, st);
   if (n <= 2048) return run_npdu_rpl<2>(p, st);
