@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -553,6 +554,245 @@ cudaError_t launch_global_sort(const float* xyz, long long batch, long long n, i
   return e != cudaSuccess ? e : e2;
 }
 
+// ---------------------------------------------------------------- device-wide radix
+// Large clouds (fp32 > 256K points, fp64 >= 64K): LSD radix over many CTAs
+// per cloud, 8-bit digits, three launches per pass -- per-tile digit
+// histograms, one exclusive scan per cloud over (digit, tile), and a stable
+// scatter. Tiles are kRadixTile consecutive keys; inside a tile, warp w owns
+// the contiguous run [w*256, w*256+256) and ranks its keys in order with
+// match.any, so the scatter preserves input order within each digit (stable,
+// as std::stable_sort). Keys are the order-preserving images of the
+// coordinates (order_key), values the storage indices.
+constexpr int kRadixThreads = 512;
+constexpr int kRadixPerThread = 8;
+constexpr int kRadixTile = kRadixThreads * kRadixPerThread;  // 4096
+
+template <typename T, typename KeyT, bool FIRST>
+__device__ __forceinline__ KeyT rs_key(const T* __restrict__ xyz, const KeyT* __restrict__ keys,
+                                       long long b, long long N, long long i, int axis) {
+  if constexpr (FIRST)
+    return order_key(xyz[(b * N + i) * 3 + axis]);
+  else
+    return keys[b * N + i];
+}
+
+template <typename T, typename KeyT, bool FIRST>
+__global__ void __launch_bounds__(kRadixThreads) rs_hist_kernel(const T* __restrict__ xyz, int axis,
+                                                                const KeyT* __restrict__ keys,
+                                                                long long N, int shift,
+                                                                uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  const long long b = blockIdx.y;
+  const int tiles = gridDim.x, tile = blockIdx.x;
+  if (threadIdx.x < 256) h[threadIdx.x] = 0;
+  __syncthreads();
+  const long long t0 = static_cast<long long>(tile) * kRadixTile;
+#pragma unroll
+  for (int e = 0; e < kRadixPerThread; ++e) {
+    const long long i = t0 + e * kRadixThreads + threadIdx.x;
+    if (i < N)
+      atomicAdd(&h[static_cast<uint32_t>(rs_key<T, KeyT, FIRST>(xyz, keys, b, N, i, axis) >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) hist[(b * 256 + threadIdx.x) * tiles + tile] = h[threadIdx.x];
+}
+
+// per (cloud, digit): exclusive scan of the digit's tile counts in place,
+// and the digit's total into totals[b][d] (the scatter scans the 256 totals)
+__global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t* __restrict__ hist,
+                                                      uint32_t* __restrict__ totals, int tiles) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t carry;
+  const long long b = blockIdx.y;
+  const int d = blockIdx.x;
+  uint32_t* h = hist + (b * 256 + d) * static_cast<long long>(tiles);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < tiles; base += 256) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < tiles ? h[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = carry;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (i < tiles) h[i] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t c = carry;
+      for (int w = 0; w < 8; ++w) c += wsum[w];
+      carry = c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[b * 256 + d] = carry;
+}
+
+// exclusive scan of 256 counters in shared memory by one warp (8 per lane)
+__device__ __forceinline__ void rs_scan256(uint32_t* c256, int lane) {
+  uint32_t c[8], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { c[q] = c256[lane * 8 + q]; sum += c[q]; }
+  uint32_t x = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  uint32_t run = x - sum;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { c256[lane * 8 + q] = run; run += c[q]; }
+}
+
+template <typename KeyT>
+constexpr size_t rs_scatter_smem() {
+  return sizeof(uint32_t) * (kRadixThreads / 32) * 256 + sizeof(uint32_t) * 512 +
+         (sizeof(KeyT) + sizeof(uint32_t)) * kRadixTile;
+}
+
+// Stable scatter of one tile: rank in order (match.any per warp), regroup
+// the tile by digit in shared memory, then write each digit's run
+// contiguously. FIRST reads the keys from the cloud (values = storage
+// indices); LAST writes the permutation and the gathered cloud instead of
+// keys/values.
+template <typename T, typename KeyT, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kRadixThreads) rs_scatter_kernel(
+    const T* __restrict__ xyz, int axis, const KeyT* __restrict__ kin,
+    const uint32_t* __restrict__ vin, long long N, int shift, const uint32_t* __restrict__ offs,
+    const uint32_t* __restrict__ totals, KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
+    T* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  constexpr int W = kRadixThreads / 32;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  KeyT* skey = reinterpret_cast<KeyT*>(rsm);
+  uint32_t* sval = reinterpret_cast<uint32_t*>(skey + kRadixTile);
+  uint32_t (*wcount)[256] = reinterpret_cast<uint32_t (*)[256]>(sval + kRadixTile);
+  uint32_t* dbase = &wcount[W - 1][0] + 256;  // digit base in the cloud
+  uint32_t* tbase = dbase + 256;               // digit base in the tile
+  const long long b = blockIdx.y;
+  const int tiles = gridDim.x, tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < W * 256; i += kRadixThreads) (&wcount[0][0])[i] = 0;
+  if (threadIdx.x < 256) dbase[threadIdx.x] = totals[b * 256 + threadIdx.x];
+  __syncthreads();
+  if (warp == 0) rs_scan256(dbase, lane);
+  const long long t0 = static_cast<long long>(tile) * kRadixTile;
+  const long long w0 = t0 + warp * (32 * kRadixPerThread);
+  const unsigned lt = (1u << lane) - 1u;
+  KeyT key[kRadixPerThread];
+  uint32_t val[kRadixPerThread], dg[kRadixPerThread], rk[kRadixPerThread];
+#pragma unroll
+  for (int r = 0; r < kRadixPerThread; ++r) {
+    const long long i = w0 + r * 32 + lane;
+    const bool valid = i < N;
+    key[r] = valid ? rs_key<T, KeyT, FIRST>(xyz, kin, b, N, i, axis) : KeyT(0);
+    val[r] = valid ? (FIRST ? static_cast<uint32_t>(i) : vin[b * N + i]) : 0u;
+    dg[r] = valid ? (static_cast<uint32_t>(key[r] >> shift) & 255u) : 256u;
+    const unsigned peers = __match_any_sync(kFull, dg[r]);
+    const uint32_t before = valid ? wcount[warp][dg[r]] : 0u;
+    rk[r] = before + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (peers & lt) == 0) wcount[warp][dg[r]] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {  // per digit: exclusive prefix over the warps, tile total
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t c = wcount[w][threadIdx.x];
+      wcount[w][threadIdx.x] = run;
+      run += c;
+    }
+    tbase[threadIdx.x] = run;
+  }
+  __syncthreads();
+  if (warp == 0) rs_scan256(tbase, lane);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRadixPerThread; ++r) {
+    if (dg[r] < 256u) {
+      const uint32_t lp = tbase[dg[r]] + wcount[warp][dg[r]] + rk[r];
+      skey[lp] = key[r];
+      sval[lp] = val[r];
+    }
+  }
+  __syncthreads();
+  const int cnt = static_cast<int>(N - t0 < kRadixTile ? N - t0 : kRadixTile);
+  const uint32_t* o = offs + b * 256LL * tiles;
+  for (int i = threadIdx.x; i < cnt; i += kRadixThreads) {
+    const uint32_t d = static_cast<uint32_t>(skey[i] >> shift) & 255u;
+    const long long dst = static_cast<long long>(dbase[d]) + o[d * tiles + tile] + (i - tbase[d]);
+    if constexpr (LAST) {
+      const uint32_t from = sval[i];
+      if (out_perm) out_perm[b * N + dst] = static_cast<int>(from);
+      if (out_xyz) gather_point(xyz + b * N * 3, out_xyz + b * N * 3, dst, from);
+    } else {
+      kout[b * N + dst] = skey[i];
+      vout[b * N + dst] = sval[i];
+    }
+  }
+}
+
+template <typename T, typename KeyT, bool FIRST, bool LAST>
+cudaError_t rs_pass(const T* xyz, int axis, const KeyT* kin, const uint32_t* vin, long long n,
+                    long long batch, long long tiles, int shift, uint32_t* hist, uint32_t* totals,
+                    KeyT* kout, uint32_t* vout, T* out_xyz, int* out_perm, cudaStream_t st) {
+  const dim3 tg(static_cast<unsigned>(tiles), static_cast<unsigned>(batch));
+  rs_hist_kernel<T, KeyT, FIRST><<<tg, kRadixThreads, 0, st>>>(xyz, axis, kin, n, shift, hist);
+  rs_scan_kernel<<<dim3(256, static_cast<unsigned>(batch)), 256, 0, st>>>(hist, totals,
+                                                                        static_cast<int>(tiles));
+  auto kern = rs_scatter_kernel<T, KeyT, FIRST, LAST>;
+  constexpr size_t smem = rs_scatter_smem<KeyT>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<tg, kRadixThreads, smem, st>>>(xyz, axis, kin, vin, n, shift, hist, totals, kout, vout,
+                                        out_xyz, out_perm);
+  return cudaGetLastError();
+}
+
+template <typename T, typename KeyT>
+cudaError_t launch_device_radix(const T* xyz, long long batch, long long n, int axis, T* out_xyz,
+                                int* out_perm, cudaStream_t st) {
+  const long long tiles = (n + kRadixTile - 1) / kRadixTile;
+  const size_t count = static_cast<size_t>(batch) * static_cast<size_t>(n);
+  const size_t bytes =
+      count * (2 * sizeof(KeyT) + 8) + sizeof(uint32_t) * 256 * (tiles + 1) * batch;
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, bytes, st);
+  if (e != cudaSuccess) return e;
+  char* p = static_cast<char*>(ws);
+  KeyT* ka = reinterpret_cast<KeyT*>(p);
+  KeyT* kb = ka + count;
+  uint32_t* va = reinterpret_cast<uint32_t*>(kb + count);
+  uint32_t* vb = va + count;
+  uint32_t* hist = vb + count;
+  uint32_t* totals = hist + 256 * tiles * batch;
+  constexpr int passes = static_cast<int>(sizeof(KeyT));
+  for (int q = 0; q < passes && e == cudaSuccess; ++q) {
+    const int shift = 8 * q;
+    if (q == 0)
+      e = rs_pass<T, KeyT, true, false>(xyz, axis, nullptr, nullptr, n, batch, tiles, shift, hist,
+                                        totals, kb, vb, nullptr, nullptr, st);
+    else if (q == passes - 1)
+      e = rs_pass<T, KeyT, false, true>(xyz, axis, ka, va, n, batch, tiles, shift, hist, totals,
+                                        nullptr, nullptr, out_xyz, out_perm, st);
+    else
+      e = rs_pass<T, KeyT, false, false>(xyz, axis, ka, va, n, batch, tiles, shift, hist, totals,
+                                         kb, vb, nullptr, nullptr, st);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  const cudaError_t e2 = cudaFreeAsync(ws, st);
+  return e != cudaSuccess ? e : e2;
+}
+
 }  // namespace pcsk
 
 namespace pcs_internal {
@@ -589,8 +829,14 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     if (n <= 4 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 4>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 8 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 8>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 16 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 16>(x, batch, n, axis, o, out_perm, stream);
-    return pcsk::launch_global_sort(x, batch, n, axis, o, out_perm, stream);
+    if (std::getenv("PCS_SORT_BITONIC"))
+      return pcsk::launch_global_sort(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_device_radix<float, uint32_t>(x, batch, n, axis, o, out_perm, stream);
   }
+  if (coord_dtype == PCS_DTYPE_F64 && n >= 65536)
+    return pcsk::launch_device_radix<double, uint64_t>(static_cast<const double*>(xyz), batch, n,
+                                                       axis, static_cast<double*>(out_xyz),
+                                                       out_perm, stream);
   // fp64 keys (drop-in path): LSD radix
   const size_t key_bytes = coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t count = static_cast<size_t>(batch) * static_cast<size_t>(n);

@@ -201,6 +201,29 @@ def test_sort_parity(pcs):
             np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
+def test_device_wide_radix_sort(pcs):
+    """Clouds past one CTA / one cluster: the multi-CTA LSD radix (fp32 >
+    256K points, fp64 >= 64K), stable with ties and signed zeros, batched."""
+    import torch
+
+    from paper_2208_08795_b200 import sort_axis
+
+    rng = np.random.default_rng(11)
+    for n, b, dt in ((262145, 2, np.float32), (1 << 20, 1, np.float32), (65536, 3, np.float64),
+                     (100003, 2, np.float64)):
+        xyz = np.round(rng.normal(size=(b, n, 3)), 3).astype(dt)
+        xyz[:, ::5, 0] = -0.0
+        xyz[:, 1::5, 0] = 0.0
+        for axis in (0, 2):
+            out, perm = sort_axis(torch.from_numpy(xyz).cuda(), axis)
+            want, order = synth.stable_sort_np(xyz, axis)
+            np.testing.assert_array_equal(perm.cpu().numpy(), order, err_msg=f"{n} {dt}")
+            np.testing.assert_array_equal(out.cpu().numpy(), want)
+    pts = synth.random_cloud(70000, 5)
+    pts[::3, 1] = pts[0, 1]
+    np.testing.assert_array_equal(pcs.exact_sort(pts, "y"), synth.stable_sort_np(pts[None], 1)[0][0])
+
+
 def test_full_size_properties_cfg4():
     """BASELINE cfg4 at full size (128 x 32768, NPDU-AFPS M=32, k=129,
     C=8192): size-independent properties on every cloud, oracle on two."""
