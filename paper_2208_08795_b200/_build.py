@@ -27,10 +27,11 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SRCS = ["full_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "morton_kernels.cu",
+           "morton_tmem_kernels.cu",
            "sample_dispatch.cu",
            "sort_kernels.cu", "metrics_kernels.cu"]
 CXX_SRCS = ["capi.cpp", "pcs_api.cpp", "io.cpp"]
-HEADERS = ["device_common.cuh", "sampler_common.cuh", "rows_common.cuh", "internal.h"]
+HEADERS = ["device_common.cuh", "sampler_common.cuh", "rows_common.cuh", "tmem.cuh", "internal.h"]
 
 
 def core_path():

@@ -36,33 +36,6 @@ namespace pcsk {
 
 using namespace rows;
 
-namespace {
-
-__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every 3rd bit
-  v &= 1023u;
-  v = (v | (v << 16)) & 0x030000FFu;
-  v = (v | (v << 8)) & 0x0300F00Fu;
-  v = (v | (v << 4)) & 0x030C30C3u;
-  v = (v | (v << 2)) & 0x09249249u;
-  return v;
-}
-
-// float <-> int with the same order (for redux / atomic min-max of floats)
-__device__ __forceinline__ int f2ord(float f) {
-  const int i = __float_as_int(f);
-  return i >= 0 ? i : i ^ 0x7fffffff;
-}
-__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
-
-// One warp's candidate as seen by every CTA of the cluster: key, sector-local
-// index, slot in the sender CTA, pivot coordinates (3 floats or 3 doubles).
-struct alignas(16) Msg {
-  uint32_t hi, lo, j, pos;
-  uint32_t c[6];
-  uint32_t pad[2];
-};
-
-}  // namespace
 
 // Local slot layout: the CTA's storage points (sector rows R % CS == rank,
 // interleaved as in rows_kernel) sorted by Morton code; slots [0, held) hold

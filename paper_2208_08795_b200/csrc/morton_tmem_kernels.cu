@@ -1,0 +1,499 @@
+// Morton-row sampler with the per-point state in tensor memory (fp32 input,
+// full window: FPS / AFPS sectors of 4K-125K points), sm_100a.
+//
+// The algorithm is morton_rows_kernel's (see morton_kernels.cu): per CTA, the
+// points regrouped into rows of 32 Morton-consecutive slots, exact box
+// pruning, lazy row keys, warp -> CTA / cluster argmax. What moves: each
+// slot's fp64 min-distance d and its sector index live in TMEM -- row r of
+// warp w is the column quad (d lo, d hi, index, -) of w's lane quarter, slot
+// position = TMEM lane -- and shared memory keeps only the fp32 coordinates
+// (12 B per point instead of 24). Consequences: an 8K-point sector fits in
+// 96 KB (two clouds per SM instead of one), a 16K-point sector fits one SM
+// (no cluster), a 32K-point sector needs a cluster of 2 instead of 4.
+//
+// TMEM is private to the warp that owns a lane quarter, so every access to a
+// row's d/index is made by the row's owner warp; rows are only ever touched
+// by their owner (row r -> warp r % W), as in the shared-memory engine.
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+#include <type_traits>
+
+#include "rows_common.cuh"
+#include "tmem.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pcsk {
+
+using namespace rows;
+
+namespace {
+
+__device__ __forceinline__ void tm_row_ld(uint32_t a, double& d, uint32_t& orig) {
+  uint32_t r[4];
+  tm_ld(a, r);
+  tm_wait_ld();
+  d = __hiloint2double(static_cast<int>(r[1]), static_cast<int>(r[0]));
+  orig = r[2];
+}
+
+}  // namespace
+
+// Slot i (row i / 32, position i % 32) -- rows interleaved over warps: local
+// row r belongs to warp r % W as its row l = r / W, stored at TMEM columns
+// tm + 4l .. 4l+3 of the warp's quarter. One row per lane for the row
+// metadata (box, max high word), as in the shared-memory engine.
+template <int W, int CS>
+__global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams p, int tm_cols) {
+  static_assert(W % 4 == 0, "whole lane quarters");
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t tm_base_sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int T = W * 32;
+  const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const long long flat = static_cast<long long>(blockIdx.x) / CS;
+  const long long b = flat / p.M, s = flat % p.M;
+  const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+  const int n = g.n;
+  const int srows = (n + 31) >> 5;
+  const int srows_local = srows > rank ? (srows - rank + CS - 1) / CS : 0;
+  const int np = p.nmax;  // slot capacity: rows_cap * 32, rows_cap = W * rpw
+  const int rpw = (np >> 5) / W;  // rows per warp (capacity)
+  float* xs = reinterpret_cast<float*>(smem);
+  float* ys = xs + np;
+  float* zs = ys + np;
+  unsigned* sampled = reinterpret_cast<unsigned*>(zs + np);
+  uint4* cand = reinterpret_cast<uint4*>(sampled + (np >> 5) + 4 - ((np >> 5) & 3));
+  Msg* xbuf = reinterpret_cast<Msg*>(cand + 2 * W);                               // [2][CS * W]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + (CS > 1 ? 2 * CS * W : 0));  // [2]
+  int* scratch = reinterpret_cast<int*>(xbar + 2);                                 // [8]
+  if (p.f64) __trap();
+  auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
+
+  if (warp == 0) tm_alloc(&tm_base_sh, tm_cols);
+  if (threadIdx.x < 6) scratch[threadIdx.x] = (threadIdx.x & 1) ? INT_MIN : INT_MAX;
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tm = tm_base_sh + ((static_cast<uint32_t>(warp & 3) * 32u) << 16) +
+                      static_cast<uint32_t>((warp >> 2) * 4 * rpw);
+  int held = 0;
+  if (srows_local > 0) {
+    const int last_R = (srows_local - 1) * CS + rank;
+    held = (srows_local - 1) * 32 + min(32, n - last_R * 32);
+  }
+  const float* cloud = static_cast<const float*>(p.xyz) + (b * p.N + g.begin) * 3;
+
+  // ---- 1. bounding box of the CTA's points (read from global / L2)
+  {
+    float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY, z0 = INFINITY,
+          z1 = -INFINITY;
+    for (int jl = threadIdx.x; jl < np; jl += T) {
+      const int gj = to_sector(jl);
+      if ((jl >> 5) < srows_local && gj < n) {
+        const float* q = cloud + 3LL * gj;
+        const float x = q[0], y = q[1], z = q[2];
+        x0 = fminf(x0, x); x1 = fmaxf(x1, x);
+        y0 = fminf(y0, y); y1 = fmaxf(y1, y);
+        z0 = fminf(z0, z); z1 = fmaxf(z1, z);
+      }
+    }
+    const int v[6] = {f2ord(x0), f2ord(x1), f2ord(y0), f2ord(y1), f2ord(z0), f2ord(z1)};
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      const int r = (a & 1) ? __reduce_max_sync(kFull, v[a]) : __reduce_min_sync(kFull, v[a]);
+      if (lane == 0) {
+        if (a & 1) atomicMax(&scratch[a], r);
+        else atomicMin(&scratch[a], r);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- 2. Morton keys (code << 32 | storage slot) over the xs/ys region
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(xs);
+  {
+    const float bx0 = ord2f(scratch[0]), by0 = ord2f(scratch[2]), bz0 = ord2f(scratch[4]);
+    const float ext = fmaxf(fmaxf(ord2f(scratch[1]) - bx0, ord2f(scratch[3]) - by0),
+                            ord2f(scratch[5]) - bz0);
+    const float sc = (ext > 0.f && ext < INFINITY) ? 1023.0f / ext : 0.f;
+    for (int jl = threadIdx.x; jl < np; jl += T) {
+      const int gj = to_sector(jl);
+      unsigned long long k = ~0ull;
+      if ((jl >> 5) < srows_local && gj < n) {
+        const float* q = cloud + 3LL * gj;
+        auto qz = [&](float c, float c0) {
+          const float t = fminf(fmaxf((c - c0) * sc, 0.f), 1023.f);
+          return spread3(static_cast<uint32_t>(t));
+        };
+        const uint32_t code = qz(q[0], bx0) | (qz(q[1], by0) << 1) | (qz(q[2], bz0) << 2);
+        k = (static_cast<unsigned long long>(code) << 32) | static_cast<uint32_t>(jl);
+      }
+      key[jl] = k;
+    }
+  }
+  __syncthreads();
+  // ---- 3. bitonic sort (non-power-of-two size: mirrored first merge step)
+  for (int kk = 2; kk < 2 * np; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      const int mask = jj == (kk >> 1) ? kk - 1 : jj;
+      for (int i = threadIdx.x; i < np; i += T) {
+        const int pi = i ^ mask;
+        if (pi > i && pi < np) {
+          const unsigned long long a = key[i], c = key[pi];
+          if (a > c) { key[i] = c; key[pi] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- 4. slot -> storage slot into the zs region, then each warp gathers
+  //         its rows' coordinates (from L2) and writes d / index to TMEM
+  {
+    uint32_t* src_slot = reinterpret_cast<uint32_t*>(zs);
+    for (int i = threadIdx.x; i < np; i += T) src_slot[i] = static_cast<uint32_t>(key[i]);
+    __syncthreads();
+    for (int l = 0; l < rpw; ++l) {
+      const int i = ((warp + W * l) << 5) + lane;
+      const uint32_t jl = src_slot[i];
+      const bool valid = i < held;
+      float x = 0.f, y = 0.f, z = 0.f;
+      uint32_t o = kNoIndex;
+      if (valid) {
+        const int gj = to_sector(static_cast<int>(jl));
+        const float* q = cloud + 3LL * gj;
+        x = q[0]; y = q[1]; z = q[2];
+        o = static_cast<uint32_t>(gj);
+      }
+      xs[i] = x; ys[i] = y; zs[i] = z;  // zs[i] overwrites src_slot[i]: same thread
+      const uint32_t w4[4] = {0u, valid ? 0x7ff00000u : 0u, o, 0u};  // d = +inf / 0
+      tm_st(tm + 4 * l, w4);
+    }
+    tm_wait_st();
+  }
+  for (int w = threadIdx.x; w < (np >> 5); w += T) sampled[w] = 0u;
+  if (p.out_sector && rank == 0)
+    for (int i = threadIdx.x; i < g.quota; i += T)
+      p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
+  bool sub_local = false;
+  if (CS > 1 && threadIdx.x == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < held; i += T)
+    sub_local |= is_subnormal_f32(xs[i]) || is_subnormal_f32(ys[i]) || is_subnormal_f32(zs[i]);
+  const bool any_sub = __syncthreads_or(sub_local) != 0;
+  if constexpr (CS > 1) cg::this_cluster().sync();
+
+  // ---- 5. per-lane row metadata: box + exact max of the high words
+  const int rows = (held + 31) >> 5;
+  const int r = warp + W * lane;  // this lane's row (the warp's row l = lane)
+  float bx0, bx1, by0, by1, bz0, bz1;
+  uint32_t rmh;
+  {
+    float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY, z0 = INFINITY,
+          z1 = -INFINITY;
+    if (r < rows) {
+      const int e = min(32, held - r * 32);
+      for (int q = 0; q < e; ++q) {
+        const int i = r * 32 + q;
+        x0 = fminf(x0, xs[i]); x1 = fmaxf(x1, xs[i]);
+        y0 = fminf(y0, ys[i]); y1 = fmaxf(y1, ys[i]);
+        z0 = fminf(z0, zs[i]); z1 = fmaxf(z1, zs[i]);
+      }
+    }
+    bx0 = x0; bx1 = x1; by0 = y0; by1 = y1; bz0 = z0; bz1 = z1;
+    rmh = r < rows ? kInfHi : 0u;
+  }
+
+  GroupSetup gs;
+  gs.b = b;
+  gs.s = s;
+  gs.g = g;
+  int cur = first_point(p, gs);  // sector-local
+  float pfx = cloud[3LL * cur], pfy = cloud[3LL * cur + 1], pfz = cloud[3LL * cur + 2];
+  double px = pfx, py = pfy, pz = pfz;
+  const long long out_base = b * p.C + g.out_off;
+  const long long index_off = g.begin + p.index_base;
+  if (rank == 0 && threadIdx.x == 0) {
+    if (p.idx64) static_cast<long long*>(p.out_idx)[out_base] = index_off + cur;
+    else static_cast<int*>(p.out_idx)[out_base] = static_cast<int>(index_off + cur);
+  }
+  for (int l = 0; l < rpw; ++l) {  // mark the first point (its unique slot)
+    double dv;
+    uint32_t o;
+    tm_row_ld(tm + 4 * l, dv, o);
+    const int i = ((warp + W * l) << 5) + lane;
+    if (o == static_cast<uint32_t>(cur)) sampled[i >> 5] |= 1u << (i & 31);
+  }
+  unsigned writes = 0;
+  int round = 0;
+
+  auto iterate = [&](auto f2f_tag) {
+  constexpr bool F2F = decltype(f2f_tag)::value;
+  for (int it = 1; it < g.quota; ++it) {
+    bool need = r < rows;
+    if (need) {
+      const float lb = __fadd_rd(__fadd_rd(gap2(bx0, bx1, pfx, pfx), gap2(by0, by1, pfy, pfy)),
+                                 gap2(bz0, bz1, pfz, pfz));
+      need = !(f32_as_f64_hi_lb(__fmul_rd(lb, 0.99999904f)) > rmh);
+    }
+    unsigned todo = __ballot_sync(kFull, need);
+    tm_wait_st();  // last iteration's row stores land before rows are re-read
+    while (todo) {
+      const int la = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int lb2 = todo ? __ffs(todo) - 1 : la;
+      todo &= todo - 1;
+      const int ja = ((warp + W * la) << 5) + lane, jb = ((warp + W * lb2) << 5) + lane;
+      uint32_t ra4[4], rb4[4];
+      tm_ld(tm + 4 * la, ra4);
+      tm_ld(tm + 4 * lb2, rb4);
+      const double ea = dist2(to_f64<F2F>(xs[ja]), to_f64<F2F>(ys[ja]), to_f64<F2F>(zs[ja]),
+                              px, py, pz);
+      const double eb = dist2(to_f64<F2F>(xs[jb]), to_f64<F2F>(ys[jb]), to_f64<F2F>(zs[jb]),
+                              px, py, pz);
+      tm_wait_ld();
+      double da = __hiloint2double(static_cast<int>(ra4[1]), static_cast<int>(ra4[0]));
+      double db = __hiloint2double(static_cast<int>(rb4[1]), static_cast<int>(rb4[0]));
+      const bool wa = ra4[2] != kNoIndex && ea <= da;
+      const bool wbb = lb2 != la && rb4[2] != kNoIndex && eb <= db;
+      writes += (wa ? 1u : 0u) + (wbb ? 1u : 0u);
+      da = wa ? ea : da;
+      db = lb2 == la ? da : (wbb ? eb : db);
+      const uint32_t sa[2] = {static_cast<uint32_t>(__double2loint(da)),
+                              static_cast<uint32_t>(__double2hiint(da))};
+      const uint32_t sb[2] = {static_cast<uint32_t>(__double2loint(db)),
+                              static_cast<uint32_t>(__double2hiint(db))};
+      tm_st(tm + 4 * la, sa);
+      tm_st(tm + 4 * lb2, sb);
+      const uint32_t ha = __reduce_max_sync(kFull, sa[1]);
+      const uint32_t hb = __reduce_max_sync(kFull, sb[1]);
+      if (lane == lb2) rmh = hb;
+      if (lane == la) rmh = ha;
+    }
+    tm_wait_st();
+    if (p.trace) {
+      for (int l = 0; l < rpw; ++l) {
+        double dv;
+        uint32_t o;
+        tm_row_ld(tm + 4 * l, dv, o);
+        if (o != kNoIndex) p.trace[static_cast<long long>(it - 1) * n + o] = dv;
+      }
+    }
+    // warp argmax: rows with the largest high word, exact key from TMEM
+    uint32_t hi = __reduce_max_sync(kFull, rmh), lo = 0u, j = kNoIndex, pos = 0u;
+    {
+      unsigned tied = __ballot_sync(kFull, r < rows && rmh == hi);
+      while (tied) {
+        const int L = __ffs(tied) - 1;
+        tied &= tied - 1;
+        double dv;
+        uint32_t o;
+        tm_row_ld(tm + 4 * L, dv, o);
+        const uint32_t h0 = static_cast<uint32_t>(__double2hiint(dv));
+        const uint32_t l0 = static_cast<uint32_t>(__double2loint(dv));
+        const uint32_t l = __reduce_max_sync(kFull, h0 == hi ? l0 : 0u);
+        const uint32_t m = __reduce_min_sync(
+            kFull, (h0 == hi && l0 == l && o != kNoIndex) ? (o << 5) | lane : kNoIndex);
+        if (l > lo || (l == lo && m < j)) {
+          lo = l; j = m; pos = (static_cast<uint32_t>(warp + W * L) << 5) | (m & 31u);
+        }
+      }
+      j = j == kNoIndex ? kNoIndex : j >> 5;
+    }
+    auto take_local = [&](uint32_t i) {
+      pfx = xs[i]; pfy = ys[i]; pfz = zs[i];
+      px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
+    };
+    constexpr unsigned kMsg = 32u;
+    auto exchange = [&](uint32_t h, uint32_t l, uint32_t jj, uint32_t at, bool& mine_out) {
+      Msg* mb = xbuf + (round & 1) * (CS * W);
+      if (lane < CS) {
+        const int i = jj == kNoIndex ? 0 : static_cast<int>(at);
+        const uint32_t rs = mapa(mb + rank * W + warp, lane), rb = mapa(&xbar[round & 1], lane);
+        st_async_v4(rs, rb, h, l, jj, at);
+        st_async_v4(rs + 16, rb, __float_as_uint(xs[i]), __float_as_uint(ys[i]),
+                    __float_as_uint(zs[i]), 0u);
+      }
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[round & 1], CS * W * kMsg);
+      mbar_wait(&xbar[round & 1], (round >> 1) & 1);
+      uint32_t bh = 0u, bl = 0u, bj = kNoIndex;
+      int be = 0;
+#pragma unroll
+      for (int e0 = 0; e0 < CS * W; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < CS * W) {
+          const uint4 k = *reinterpret_cast<const uint4*>(mb + e);
+          if (key_gt(k.x, k.y, k.z, bh, bl, bj)) { bh = k.x; bl = k.y; bj = k.z; be = e; }
+        }
+      }
+      uint32_t h2 = bh, l2 = bl, j2 = bj;
+      warp_argmax(h2, l2, j2);
+      const unsigned who = __ballot_sync(kFull, bh == h2 && bl == l2 && bj == j2);
+      const int e = __shfl_sync(kFull, be, __ffs(who) - 1);
+      const Msg& w = mb[e];
+      pfx = __uint_as_float(w.c[0]); pfy = __uint_as_float(w.c[1]); pfz = __uint_as_float(w.c[2]);
+      px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
+      mine_out = e / W == rank;
+      pos = w.pos;
+      hi = h2; lo = l2; j = j2;
+      ++round;
+    };
+    bool mine = true;
+    if constexpr (CS > 1) {
+      exchange(hi, lo, j, pos, mine);
+    } else {
+      uint4* buf = cand + (round & 1) * W;
+      if (lane == 0) buf[warp] = make_uint4(hi, lo, j, pos);
+      __syncthreads();
+      const uint4 v = lane < W ? buf[lane] : make_uint4(0, 0, kNoIndex, 0);
+      hi = v.x; lo = v.y; j = v.z;
+      warp_argmax(hi, lo, j);
+      const unsigned who = __ballot_sync(kFull, lane < W && v.x == hi && v.y == lo && v.z == j);
+      pos = buf[who ? __ffs(who) - 1 : 0].w;
+      ++round;
+      if ((hi | lo) != 0u) take_local(pos);
+    }
+    if ((hi | lo) == 0u) {
+      // every distance is 0: lowest unsampled index (sampler.cpp:148-154);
+      // each warp scans its own rows, then the CTA combines
+      uint32_t jm = kNoIndex, at = 0u;
+      for (int l = 0; l < rpw; ++l) {
+        double dv;
+        uint32_t o;
+        tm_row_ld(tm + 4 * l, dv, o);
+        const int i = ((warp + W * l) << 5) + lane;
+        const bool free_slot = i < held && !((sampled[i >> 5] >> (i & 31)) & 1u);
+        if (free_slot && o < jm) { jm = o; at = static_cast<uint32_t>(i); }
+      }
+      const uint32_t wm = __reduce_min_sync(kFull, jm);
+      const unsigned who = __ballot_sync(kFull, jm == wm);
+      at = __shfl_sync(kFull, at, __ffs(who) - 1);
+      uint4* buf = cand + (round & 1) * W;
+      if (lane == 0) buf[warp] = make_uint4(wm, at, 0, 0);
+      __syncthreads();
+      const uint4 v = lane < W ? buf[lane] : make_uint4(kNoIndex, 0, 0, 0);
+      jm = __reduce_min_sync(kFull, v.x);
+      const unsigned who2 = __ballot_sync(kFull, lane < W && v.x == jm);
+      at = __shfl_sync(kFull, v.y, __ffs(who2) - 1);
+      ++round;
+      if constexpr (CS > 1) {
+        exchange(jm != kNoIndex ? 1u : 0u, 0u, jm, at, mine);
+      } else {
+        j = jm;
+        pos = at;
+        take_local(at);
+      }
+    }
+    cur = static_cast<int>(j);
+    if (rank == 0 && threadIdx.x == 0) {
+      if (p.idx64) static_cast<long long*>(p.out_idx)[out_base + it] = index_off + cur;
+      else static_cast<int*>(p.out_idx)[out_base + it] = static_cast<int>(index_off + cur);
+    }
+    if (mine && threadIdx.x == 0) sampled[pos >> 5] |= 1u << (pos & 31);
+  }
+  };
+  if (any_sub)
+    iterate(std::true_type{});
+  else
+    iterate(std::false_type{});
+  const unsigned ws = __reduce_add_sync(kFull, writes);
+  if (p.stats) {
+    unsigned long long* st = p.stats + b * 4;
+    if (lane == 0 && ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
+    if (rank == 0 && threadIdx.x == 0) {
+      const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
+      atomicAdd(st + 0, iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 3, iters);
+    }
+  }
+  tm_wait_st();
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) tm_dealloc(tm_base_sh, tm_cols);
+  if constexpr (CS > 1) cg::this_cluster().sync();
+}
+
+namespace {
+
+size_t morton_tmem_smem(int np, int W, int CS) {
+  size_t bytes = static_cast<size_t>(np) * 12;
+  bytes += ((np >> 5) + 4 - ((np >> 5) & 3)) * 4;
+  bytes += 2 * W * sizeof(uint4);
+  bytes += CS > 1 ? 2 * CS * W * sizeof(Msg) : 0;
+  bytes += 2 * sizeof(uint64_t) + 8 * sizeof(int);
+  return bytes;
+}
+
+template <int W, int CS>
+cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
+  const int rpw = (rows + W - 1) / W;
+  const int np = rpw * W * 32;
+  p.nmax = np;
+  const size_t smem = morton_tmem_smem(np, W, CS);
+  if (smem > kMaxSmem) return cudaErrorNotSupported;
+  int cols = 32;
+  while (cols < W * rpw) cols *= 2;  // W/4 warps per quarter x 4 columns x rpw rows
+  if (cols > 512) return cudaErrorNotSupported;
+  auto kern = morton_tmem_kernel<W, CS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.B * p.M * CS));
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p, cols);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <int CS>
+cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
+  // one row per lane: W >= rows / 32, a multiple of 4 (whole lane quarters)
+  if (rows <= 128) return launch_morton_tmem<4, CS>(p, rows, st);
+  if (rows <= 256) return launch_morton_tmem<8, CS>(p, rows, st);
+  if (rows <= 512) return launch_morton_tmem<16, CS>(p, rows, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory).
+cudaError_t run_morton_tmem_any(SampleParams p, long long n, cudaStream_t st) {
+  if (p.f64) return cudaErrorNotSupported;
+  const long long srows = (n + 31) / 32;
+  for (int CS = 1; CS <= 16; CS *= 2) {
+    const int rows = static_cast<int>((srows + CS - 1) / CS);
+    if (rows > 512) continue;
+    const int W = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
+    const int rpw = (rows + W - 1) / W;
+    if (morton_tmem_smem(rpw * W * 32, W, CS) > kMaxSmem) continue;
+    switch (CS) {
+      case 1: return launch_morton_tmem_w<1>(p, rows, st);
+      case 2: return launch_morton_tmem_w<2>(p, rows, st);
+      case 4: return launch_morton_tmem_w<4>(p, rows, st);
+      case 8: return launch_morton_tmem_w<8>(p, rows, st);
+      default: return launch_morton_tmem_w<16>(p, rows, st);
+    }
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace pcsk

@@ -22,6 +22,7 @@
 #include <type_traits>
 
 #include "sampler_common.cuh"
+#include "tmem.cuh"
 
 namespace pcsk {
 
@@ -313,34 +314,7 @@ cudaError_t run_npdu_rpl(SampleParams p, cudaStream_t st) {
 // pair (2r, 2r+1) = (lo, hi) words of each lane's double. A window's RMAX rows
 // are one or two tcgen05.ld/st per iteration.
 
-__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[2]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
-               : "=r"(r[0]), "=r"(r[1]) : "r"(a));
-}
-__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[4]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
-}
-__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                 "=r"(r[6]), "=r"(r[7]) : "r"(a));
-}
-__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[2]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};"
-               :: "r"(a), "r"(r[0]), "r"(r[1]) : "memory");
-}
-__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[4]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
-               :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
-}
-__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
-               :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
-                  "r"(r[6]), "r"(r[7]) : "memory");
-}
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 
 // RMAX rows = 2*RMAX columns, as power-of-two tcgen05 shapes
 template <int RMAX>

@@ -23,11 +23,19 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   const bool use_morton = !windowed && !(morton && std::string(morton) == "0");
   const char* mmin = std::getenv("PCS_MORTON_MIN");
   const long long morton_min = mmin ? std::atoll(mmin) : kMortonMin;
+  // fp32 input: the TMEM form first (per-point state in tensor memory, half
+  // the shared memory per point); PCS_MORTON_TMEM=0 keeps it in shared memory
+  const char* mt = std::getenv("PCS_MORTON_TMEM");
+  const bool morton_tmem = !p.f64 && !(mt && std::string(mt) == "0");
+  auto morton_any = [&]() {
+    cudaError_t r = morton_tmem ? run_morton_tmem_any(p, nmax_sector, st) : cudaErrorNotSupported;
+    return r == cudaErrorNotSupported ? run_morton_any(p, nmax_sector, st) : r;
+  };
   cudaError_t e = cudaErrorNotSupported;
-  if (use_morton && (rows || nmax_sector > morton_min)) e = run_morton_any(p, nmax_sector, st);
+  if (use_morton && (rows || nmax_sector > morton_min)) e = morton_any();
   if (e == cudaErrorNotSupported && !rows)
     e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
-  if (e == cudaErrorNotSupported && use_morton) e = run_morton_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && use_morton) e = morton_any();
   if (e == cudaErrorNotSupported) e = run_rows_any(p, nmax_sector, windowed, st);
   if (e == cudaErrorNotSupported && msg)
     *msg = "sector of " + std::to_string(nmax_sector) +

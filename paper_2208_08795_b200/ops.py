@@ -210,6 +210,23 @@ def _morton_fits(n: int, dtype: str) -> bool:
     return False
 
 
+def _morton_tmem_fits(n: int) -> bool:
+    """Mirror of run_morton_tmem_any (csrc/morton_tmem_kernels.cu), fp32."""
+    srows = -(-n // 32)
+    for cs in (1, 2, 4, 8, 16):
+        rows = -(-srows // cs)
+        if rows > 512:
+            continue
+        w = 4 if rows <= 128 else 8 if rows <= 256 else 16
+        np_ = -(-rows // w) * w * 32
+        nbytes = np_ * 12 + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
+        nbytes += 2 * cs * w * 48 if cs > 1 else 0
+        nbytes += 2 * 8 + 8 * 4
+        if nbytes <= 227 * 1024:
+            return True
+    return False
+
+
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None, dtype: str = "float32") -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
@@ -226,6 +243,9 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
               and _morton_fits(nmax, dtype))
     if morton and (rows or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
+        if dtype != "float64" and os.environ.get("PCS_MORTON_TMEM", "1") != "0" and \
+                _morton_tmem_fits(nmax):
+            return "morton_tmem_kernel"
         return "morton_rows_kernel"
     if rows:
         return "rows_kernel"

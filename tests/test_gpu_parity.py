@@ -126,7 +126,7 @@ def test_distance_trace_bit_exact(pcs, oracle):
 @pytest.mark.parametrize("morton", ["1", "0"])
 def test_distance_trace_rows_engines(pcs, oracle, monkeypatch, morton):
     """Trace through the pruned-row engines (the Morton engine writes d[] back
-    through its slot -> index map)."""
+    through its slot -> index map; the trace entry is the fp64 drop-in)."""
     monkeypatch.setenv("PCS_SAMPLER", "rows")
     monkeypatch.setenv("PCS_MORTON", morton)
     pts = synth.random_cloud(700, 405)
@@ -330,14 +330,20 @@ def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("tmem", ["1", "0"])
 @pytest.mark.parametrize("cloud", ["cube", "primitives", "dupes", "f64"])
-def test_morton_rows_large_sectors(pcs, oracle, cloud):
-    """Full-window sectors past 4096 points take the Morton-row engine (CTA
-    Morton sort, orig-index row keys): one CTA at 8K, clusters of 2/4/8 at
-    16K/32K/60K; clustered, duplicated and fp64 inputs; random starts."""
+def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
+    """Full-window sectors past 3072 points take the Morton-row engines (CTA
+    Morton sort, orig-index row keys; per-point state in TMEM for fp32 input,
+    or in shared memory): one CTA up to 8K/16K, clusters beyond; clustered,
+    duplicated and fp64 inputs; random starts."""
     import torch
 
     from paper_2208_08795_b200 import sample
+
+    monkeypatch.setenv("PCS_MORTON_TMEM", tmem)
+    if cloud == "f64" and tmem == "0":
+        pytest.skip("fp64 input always uses the shared-memory engine")
 
     for n, c, m in ((8192, 2048, 1), (16384, 1500, 1), (32768, 700, 1), (60000, 300, 1),
                     (40000, 4000, 4)):
