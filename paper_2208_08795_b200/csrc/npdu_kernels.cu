@@ -22,6 +22,7 @@
 #include <type_traits>
 
 #include "sampler_common.cuh"
+#include "rows_common.cuh"
 #include "tmem.cuh"
 
 namespace pcsk {
@@ -384,7 +385,8 @@ __host__ __device__ constexpr size_t tm_warp_smem(int ncap) {
 // fp32 input, sectors <= NCAP <= 1024 points (one row maximum per lane)
 template <int RMAX, int NCAP>
 __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
-  static_assert(NCAP >= 32 * RMAX && NCAP <= 1024, "capacity");
+  static_assert(NCAP >= 32 * RMAX && NCAP <= 4096, "capacity");
+  constexpr int RPL = NCAP > 1024 ? NCAP / 1024 : 1;  // rows per lane (row r: lane r % 32)
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tm_base_sh;
   const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -429,8 +431,14 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     if (p.out_sector)
       for (int i = lane; i < g.quota; i += 32)
         p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
-    uint32_t rm_hi = lane < rows ? kInfHi : 0u, rm_lo = 0u;
-    uint32_t rm_j = lane < rows ? static_cast<uint32_t>(lane * 32) : kNoIndex;
+    uint32_t rm_hi[RPL], rm_lo[RPL], rm_j[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      rm_hi[i] = r < rows ? kInfHi : 0u;
+      rm_lo[i] = 0u;
+      rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
+    }
     GroupSetup gs;
     gs.b = b;
     gs.s = s;
@@ -490,11 +498,7 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       for (int q = 0; q < RMAX; ++q) {
         uint32_t hi, lo, jj;
         row_key(dj[q], r_lo + q, hi, lo, jj);
-        if (r_lo + q == lane) {
-          rm_hi = hi;
-          rm_lo = lo;
-          rm_j = jj;
-        }
+        store_row<RPL>(r_lo + q, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
       }
       if (trace) {
         tm_wait_st();
@@ -508,7 +512,12 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
                 __hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0]));
         }
       }
-      uint32_t hi = rm_hi, lo = rm_lo, j = rm_j;
+      uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
+#pragma unroll
+      for (int i = 1; i < RPL; ++i)
+        if (rows::key_gt(rm_hi[i], rm_lo[i], rm_j[i], hi, lo, j)) {
+          hi = rm_hi[i]; lo = rm_lo[i]; j = rm_j[i];
+        }
       warp_argmax(hi, lo, j);
       if ((hi | lo) == 0u) {
         // fold outputs [marked, it) into the bitmap: whole blocks from
@@ -585,12 +594,14 @@ cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
   const char* tmv = std::getenv("PCS_NPDU_TMEM");
   const bool use_tmem = !(tmv && tmv[0] == '0');
   const long long rows_needed = (p.K + 62) / 32;
-  if (use_tmem && !p.f64 && n <= 1024 && rows_needed <= 5) {
+  if (use_tmem && !p.f64 && n <= 4096 && rows_needed <= 5) {
     auto by_cap = [&](auto rmax_tag) {
       constexpr int R = decltype(rmax_tag)::value;
       if (n <= 256) return run_npdu_tmem<R, 256>(p, st);
       if (n <= 512) return run_npdu_tmem<R, 512>(p, st);
-      return run_npdu_tmem<R, 1024>(p, st);
+      if (n <= 1024) return run_npdu_tmem<R, 1024>(p, st);
+      if (n <= 2048) return run_npdu_tmem<R, 2048>(p, st);
+      return run_npdu_tmem<R, 4096>(p, st);
     };
     if (rows_needed <= 2) return by_cap(std::integral_constant<int, 2>{});
     if (rows_needed <= 3) return by_cap(std::integral_constant<int, 3>{});

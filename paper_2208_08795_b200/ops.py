@@ -250,7 +250,7 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     if rows:
         return "rows_kernel"
     if windowed:
-        if nmax <= 1024 and (k + 62) // 32 <= 5 and dtype != "float64" and \
+        if nmax <= 4096 and (k + 62) // 32 <= 5 and dtype != "float64" and \
                 os.environ.get("PCS_NPDU_TMEM", "1") != "0":
             return "npdu_tmem_kernel"
         return "npdu_warp_kernel" if nmax <= 8192 else "rows_kernel"

@@ -370,7 +370,7 @@ def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
 
 @pytest.mark.parametrize("index_dtype", ["int32", "int64"])
 def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
-    """fp32 NPDU sectors <= 1024 points (the TMEM kernel): heavily duplicated
+    """fp32 NPDU sectors <= 4096 points (the TMEM kernel, 1-4 rows per lane): heavily duplicated
     clouds drive the all-zero slow path (lowest unsampled index) many times;
     quotas that are not multiples of 32 exercise the buffered output flush."""
     import torch
@@ -379,7 +379,8 @@ def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
 
     rng = np.random.default_rng(9)
     for n, c, m, k in ((4096, 1232, 4, 129), (3000, 2995, 3, 65), (1024, 77, 1, 33),
-                       (2048, 2048, 2, 97)):
+                       (2048, 2048, 2, 97), (8192, 2001, 2, 129), (6000, 1500, 3, 65),
+                       (4000, 999, 1, 33)):
         xyz = synth.uniform_cube(3, n, n)
         xyz[0] = xyz[0][rng.integers(0, 40, n)]            # 40 distinct points
         xyz[1, : n // 2] = xyz[1, 7]                        # half coincident
