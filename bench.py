@@ -52,8 +52,10 @@ for _n in (2048, 4096, 8192, 16384, 32768):
     WORKLOADS[f"cfg5-npdu-{_n}"] = dict(gen="cube", B=256, N=_n, method="npdu_afps", C=_n // 4,
                                         M=16, K=65, sort="x")
 
+# one 1M-point cloud: under torchrun its sectors are split across the ranks
+# (strong scaling, BASELINE cfg5), each rank sorting the cloud itself
 WORKLOADS["cfg5-1m"] = dict(gen="cube", B=1, N=1 << 20, method="afps", C=(1 << 20) // 4, M=1024,
-                            K=None, sort="x")
+                            K=None, sort="x", strong=True)
 
 # latency probes: one NPDU sector per warp, 1 warp / 148 warps / 4096 warps
 for _b in (1, 148, 4096):
@@ -186,6 +188,17 @@ def _cpu_model():
     return "unknown"
 
 
+def launches_per_step(w):
+    """Our kernels per step (csrc/sort_kernels.cu, csrc/sample_dispatch.cu):
+    one sampler launch; the axis sort is one launch up to 256K fp32 points,
+    otherwise the device-wide radix (histogram, scan, scatter per 8-bit
+    pass)."""
+    sort = 0
+    if w["sort"]:
+        sort = 1 if w["N"] <= 16 * 16384 else 3 * 4
+    return 1 + sort
+
+
 def host_sorted(w, xyz):
     if w["sort"] is None:
         return xyz
@@ -241,14 +254,29 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     args.warmup = max(args.warmup, 3)
 
-    # each rank gets its own clouds (weak scaling): seed by rank
-    xyz_host = make_input(w, seed_base=1000 * rank)
+    # weak scaling: each rank gets its own clouds (seeded by rank); strong
+    # (one cloud, world > 1): every rank holds the same cloud, sorts it, and
+    # samples its contiguous run of sectors with global index / sector bases
+    strong = bool(w.get("strong")) and world > 1
+    xyz_host = make_input(w, seed_base=0 if strong else 1000 * rank)
     xyz = torch.from_numpy(xyz_host).to(dev)
     B, N, C = w["B"], w["N"], w["C"]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    from paper_2208_08795_b200 import shard
+
+    sh = shard.sector_shard(N, C, w["M"], world, rank) if strong else None
+
+    def sample_sorted(xs):
+        if sh is None:
+            return pcs.sample(xs, C, method=w["method"], m=w["M"], k=w["K"])
+        return pcs.sample(xs[:, sh.point_lo:sh.point_hi], sh.c, method=w["method"], m=sh.m,
+                          k=w["K"], index_base=sh.point_lo, sector_base=sh.sector_lo)
 
     def step(x):
-        return pcs.sample(x, C, method=w["method"], m=w["M"], k=w["K"], sort=w["sort"])
+        if sh is None:
+            return pcs.sample(x, C, method=w["method"], m=w["M"], k=w["K"], sort=w["sort"])
+        xs = pcs.sort_axis(x, w["sort"])[0] if w["sort"] else x
+        return sample_sorted(xs)
 
     for _ in range(args.warmup):
         out = step(xyz)
@@ -277,7 +305,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_per_step = ms / args.steps
-    pts_per_s = world * B * C / (ms_per_step * 1e-3)
+    total_samples = B * C if strong else world * B * C
+    pts_per_s = total_samples / (ms_per_step * 1e-3)
 
     # ---- sampler kernel alone (roofline): sort once, time only the sampler
     xs = pcs.sort_axis(xyz, w["sort"])[0] if w["sort"] else xyz
@@ -286,7 +315,7 @@ def main():
     for i in range(args.steps):
         flush.fill_(float(i))
         ks.record()
-        pcs.sample(xs, C, method=w["method"], m=w["M"], k=w["K"])
+        sample_sorted(xs)
         ke.record()
         torch.cuda.synchronize()
         kern_ms += ks.elapsed_time(ke)
@@ -312,10 +341,20 @@ def main():
         def e2e_step():
             # the public API with host buffers: pinned batch in, host results
             # out (pipelined H2D / sort+sample / D2H inside the call)
-            return pcs.sample(pinned, C, method=w["method"], m=w["M"], k=w["K"], sort=w["sort"])
+            if sh is None:
+                return pcs.sample(pinned, C, method=w["method"], m=w["M"], k=w["K"],
+                                  sort=w["sort"])
+            res = step(pinned.to(dev, non_blocking=True))
+            return tuple(t.cpu() for t in res)
 
-        for _ in range(args.warmup):
+        # warm-up: at least W steps and 0.5 s -- the host link ramps up over
+        # the first ~15 transfers after idling (1.6-3 ms -> 1.2 ms per step
+        # measured, tools/e2e_dbg.py)
+        t_warm = time.perf_counter()
+        for i in range(max(args.warmup, 1000)):
             e2e_step()
+            if i + 1 >= args.warmup and time.perf_counter() - t_warm > 0.5:
+                break
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -343,7 +382,7 @@ def main():
             torch.cuda.synchronize()
             h2d.append(es.elapsed_time(ee))
         del dst
-        e2e = {"value": world * B * C / (e_ms * 1e-3), "unit": "sampled points/s",
+        e2e = {"value": total_samples / (e_ms * 1e-3), "unit": "sampled points/s",
                "ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
                "h2d_gbps": pinned.numel() * pinned.element_size() / min(h2d) / 1e6,
                "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
@@ -364,14 +403,16 @@ def main():
         line = {
             "metric": "sampled points/s", "value": pts_per_s, "unit": "sampled points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "clouds_per_s": world * B / (ms_per_step * 1e-3),
+            "clouds_per_s": (B if strong else world * B) / (ms_per_step * 1e-3),
             "config": {"workload": args.workload, "clouds_per_gpu": B, "points_per_cloud": N,
                        "samples_per_cloud": C, "method": w["method"], "m": w["M"], "k": w["K"],
                        "sort": w["sort"], "generator": w["gen"], "coords": "fp32 in, fp64 math",
-                       "l2": "flushed between steps (512 MiB write)", "parallelism": f"dp{world}"},
-            "gpu_launches": args.steps * (2 if w["sort"] else 1),
+                       "l2": "flushed between steps (512 MiB write)",
+                       "parallelism": (f"sector-split x{world}" if strong else f"dp{world}")},
+            "gpu_launches": args.steps * launches_per_step(w),
             "dist_evals_per_step": evals_per_step,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clocks.summary(),
