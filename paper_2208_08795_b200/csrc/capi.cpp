@@ -3,6 +3,7 @@
 // reference-facing bindings call.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -10,6 +11,24 @@
 #include "pcs_gpu.h"
 
 namespace pcs_internal {
+
+cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static std::atomic<unsigned long long> retained{0};  // bit per device (< 64)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+  if (bit && !(retained.load() & bit)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    retained.fetch_or(bit);
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 namespace {
 thread_local std::string g_error;
 
@@ -37,7 +56,9 @@ struct DevBuf {
   void* p = nullptr;
   cudaStream_t s;
   explicit DevBuf(cudaStream_t st) : s(st) {}
-  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes ? bytes : 16, s); }
+  cudaError_t alloc(size_t bytes) {
+    return pcs_internal::workspace_alloc(&p, bytes ? bytes : 16, s);
+  }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);
   }

@@ -3,6 +3,13 @@
 
 #include "sampler_common.cuh"
 
+#ifdef PCS_PROF
+__device__ unsigned long long g_fprof[8];
+#define FPROF_T(v) long long v = clock64()
+#else
+#define FPROF_T(v)
+#endif
+
 namespace pcsk {
 
 // ---------------------------------------------------------------- full window
@@ -37,12 +44,33 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
   }
 
   int cur = first_point(p, gs);
-  if (t == 0) write_index(p, gs.b, gs.g.out_off, gs.g.begin + cur);
+  // output indices buffered in warp 0, sample i in lane i % 32, stored 32 at
+  // a time (off the iteration's critical path)
+  const long long obase = gs.b * p.C + gs.g.out_off;
+  const long long ioff = gs.g.begin + p.index_base;
+  const bool idx64 = p.idx64 != 0;
+  void* const out = p.out_idx;
+  // (measured: a win for 1-4 warps per sector, a loss with 8+ where the
+  // extra state changes the compiler's schedule of the slot loop)
+  constexpr bool kBufOut = W <= 4;
+  int ob = cur;
+  if (!kBufOut && t == 0) write_index(p, gs.b, gs.g.out_off, gs.g.begin + cur);
+  auto flush = [&](int i0, int cnt) {
+    if (warp == 0 && lane < cnt) {
+      if (idx64) static_cast<long long*>(out)[obase + i0 + lane] = ioff + ob;
+      else static_cast<int*>(out)[obase + i0 + lane] = static_cast<int>(ioff + ob);
+    }
+  };
   unsigned smask = (cur % T == t) ? (1u << (cur / T)) : 0u;
+  double* const trace = p.trace;
   unsigned writes = 0;
   int round = 0;
 
+#ifdef PCS_PROF
+  unsigned long long pacc[4] = {0, 0, 0, 0};
+#endif
   for (int it = 1; it < gs.g.quota; ++it) {
+    FPROF_T(t0);
     const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
     unsigned long long best = 0;
     int bs = -1;
@@ -66,20 +94,37 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
         bs = k;
       }
     }
-    if (p.trace) {
+    if (trace) {
 #pragma unroll
       for (int k = 0; k < P; ++k)
-        if ((vmask >> k) & 1u) p.trace[static_cast<long long>(it - 1) * n + k * T + t] = d[k];
+        if ((vmask >> k) & 1u) trace[static_cast<long long>(it - 1) * n + k * T + t] = d[k];
     }
+    FPROF_T(t1);
     uint32_t hi = static_cast<uint32_t>(best >> 32), lo = static_cast<uint32_t>(best);
     uint32_t j = bs >= 0 ? static_cast<uint32_t>(bs * T + t) : kNoIndex;
     group_argmax<W>(hi, lo, j, gs.cand, round, gid, lane, warp);
+    FPROF_T(t2);
     if ((hi | lo) == 0u)
       j = lowest_unsampled<P, W>(vmask, smask, t, gs.cand, round, gid, lane, warp);
     cur = static_cast<int>(j);
-    if (t == 0) write_index(p, gs.b, gs.g.out_off + it, gs.g.begin + cur);
+    if constexpr (kBufOut) {
+      if (lane == (it & 31)) ob = cur;
+      if ((it & 31) == 31) flush(it - 31, 32);
+    } else if (t == 0) {
+      write_index(p, gs.b, gs.g.out_off + it, gs.g.begin + cur);
+    }
     if (cur % T == t) smask |= 1u << (cur / T);
+#ifdef PCS_PROF
+    FPROF_T(t3);
+    pacc[0] += t1 - t0; pacc[1] += t2 - t1; pacc[2] += t3 - t2; pacc[3] += 1;
+#endif
   }
+#ifdef PCS_PROF
+  if (t == 0)
+    for (int q = 0; q < 4; ++q) atomicAdd(&g_fprof[q], pacc[q]);
+#endif
+  if (kBufOut && ((gs.g.quota - 1) & 31) != 31)
+    flush((gs.g.quota - 1) & ~31, ((gs.g.quota - 1) & 31) + 1);
   const unsigned long long evals =
       static_cast<unsigned long long>(gs.g.quota - 1) * static_cast<unsigned long long>(n);
   flush_stats<W>(p, gs, t, writes, evals);

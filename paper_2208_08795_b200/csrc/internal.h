@@ -10,6 +10,12 @@
 
 namespace pcs_internal {
 
+// Stream-ordered workspace from the device's default memory pool, which is
+// set (once per device) to keep freed memory instead of returning it to the
+// driver at every synchronisation -- otherwise each call re-maps its
+// workspace (measured: a 1M-point sort 0.27 ms warm vs 0.48 ms re-mapped).
+cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t st);
+
 // Argument validation in the reference's order with its exact messages
 // (proj/src/sampler.cpp:20-23 check_sample_count, proj/src/sectors.cpp:9-51
 // SectorPlan::make, proj/src/sampler.cpp:89-94 local_fps). Returns PCS_OK

@@ -127,7 +127,7 @@ template <typename T, typename I>
 cudaError_t run_metric(int which, const void* xyz, long long B, long long N, const void* idx,
                        long long C, double* out, cudaStream_t st) {
   unsigned long long* bits = nullptr;
-  cudaError_t e = cudaMallocAsync(&bits, sizeof(unsigned long long) * B, st);
+  cudaError_t e = pcs_internal::workspace_alloc(reinterpret_cast<void**>(&bits), sizeof(unsigned long long) * B, st);
   if (e != cudaSuccess) return e;
   // coverage starts at 0 (max), separation at +inf (min)
   fill_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, st>>>(

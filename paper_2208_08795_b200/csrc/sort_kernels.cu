@@ -531,7 +531,7 @@ cudaError_t launch_global_sort(const float* xyz, long long batch, long long n, i
   long long T = kBlk;
   while (T < n) T <<= 1;
   unsigned long long* keys = nullptr;
-  cudaError_t e = cudaMallocAsync(&keys, sizeof(unsigned long long) * T * batch, st);
+  cudaError_t e = pcs_internal::workspace_alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * T * batch, st);
   if (e != cudaSuccess) return e;
   const size_t smem = sizeof(unsigned long long) * kBlk;
   e = cudaFuncSetAttribute(block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -765,7 +765,7 @@ cudaError_t launch_device_radix(const T* xyz, long long batch, long long n, int 
   const size_t bytes =
       count * (2 * sizeof(KeyT) + 8) + sizeof(uint32_t) * 256 * (tiles + 1) * batch;
   void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, bytes, st);
+  cudaError_t e = pcs_internal::workspace_alloc(reinterpret_cast<void**>(&ws), bytes, st);
   if (e != cudaSuccess) return e;
   char* p = static_cast<char*>(ws);
   KeyT* ka = reinterpret_cast<KeyT*>(p);
@@ -841,7 +841,7 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   const size_t key_bytes = coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t count = static_cast<size_t>(batch) * static_cast<size_t>(n);
   void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, count * (2 * key_bytes + 8), stream);
+  cudaError_t e = pcs_internal::workspace_alloc(reinterpret_cast<void**>(&ws), count * (2 * key_bytes + 8), stream);
   if (e != cudaSuccess) return e;
   char* p = static_cast<char*>(ws);
   void* ka = p;
