@@ -24,6 +24,13 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef PCS_PROF
+__device__ unsigned long long g_tprof[8];
+#define TPROF_T(v) long long v = clock64()
+#else
+#define TPROF_T(v)
+#endif
+
 namespace pcsk {
 
 using namespace rows;
@@ -230,10 +237,14 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   }
   unsigned writes = 0;
   int round = 0;
+#ifdef PCS_PROF
+  unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
   auto iterate = [&](auto f2f_tag) {
   constexpr bool F2F = decltype(f2f_tag)::value;
   for (int it = 1; it < g.quota; ++it) {
+    TPROF_T(t0);
     bool need = r < rows;
     if (need) {
       const float lb = __fadd_rd(__fadd_rd(gap2(bx0, bx1, pfx, pfx), gap2(by0, by1, pfy, pfy)),
@@ -241,8 +252,14 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       need = !(f32_as_f64_hi_lb(__fmul_rd(lb, 0.99999904f)) > rmh);
     }
     unsigned todo = __ballot_sync(kFull, need);
+#ifdef PCS_PROF
+    pacc[4] += __popc(todo);
+#endif
     tm_wait_st();  // last iteration's row stores land before rows are re-read
     while (todo) {
+#ifdef PCS_PROF
+      pacc[5] += 1;
+#endif
       const int la = __ffs(todo) - 1;
       todo &= todo - 1;
       const int lb2 = todo ? __ffs(todo) - 1 : la;
@@ -283,6 +300,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
         if (o != kNoIndex) p.trace[static_cast<long long>(it - 1) * n + o] = dv;
       }
     }
+    TPROF_T(t1);
     // warp argmax: rows with the largest high word, exact key from TMEM
     uint32_t hi = __reduce_max_sync(kFull, rmh), lo = 0u, j = kNoIndex, pos = 0u;
     {
@@ -304,6 +322,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       }
       j = j == kNoIndex ? kNoIndex : j >> 5;
     }
+    TPROF_T(t2);
     auto take_local = [&](uint32_t i) {
       pfx = xs[i]; pfy = ys[i]; pfz = zs[i];
       px = to_f64<F2F>(pfx); py = to_f64<F2F>(pfy); pz = to_f64<F2F>(pfz);
@@ -357,6 +376,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       ++round;
       if ((hi | lo) != 0u) take_local(pos);
     }
+    TPROF_T(t3);
     if ((hi | lo) == 0u) {
       // every distance is 0: lowest unsampled index (sampler.cpp:148-154);
       // each warp scans its own rows, then the CTA combines
@@ -394,12 +414,20 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       else static_cast<int*>(p.out_idx)[out_base + it] = static_cast<int>(index_off + cur);
     }
     if (mine && threadIdx.x == 0) sampled[pos >> 5] |= 1u << (pos & 31);
+#ifdef PCS_PROF
+    TPROF_T(t4);
+    pacc[0] += t1 - t0; pacc[1] += t2 - t1; pacc[2] += t3 - t2; pacc[3] += t4 - t3;
+#endif
   }
   };
   if (any_sub)
     iterate(std::true_type{});
   else
     iterate(std::false_type{});
+#ifdef PCS_PROF
+  if (lane == 0)
+    for (int q = 0; q < 6; ++q) atomicAdd(&g_tprof[q], pacc[q]);
+#endif
   const unsigned ws = __reduce_add_sync(kFull, writes);
   if (p.stats) {
     unsigned long long* st = p.stats + b * 4;

@@ -392,6 +392,21 @@ def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
             np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+def test_sector_beyond_on_chip_engines_is_an_error():
+    """No host fallback: a full-window sector larger than every on-chip
+    engine holds is reported, not sampled on the CPU."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = torch.from_numpy(synth.uniform_cube(1, 300000, 3)).cuda()
+    with pytest.raises((RuntimeError, ValueError), match="exceeds the on-chip samplers"):
+        sample(xyz, 1000, method="fps")
+    # the same cloud as 4 AFPS sectors is fine
+    idx, st = sample(xyz, 1000, method="afps", m=4)
+    assert len(np.unique(idx.cpu().numpy())) == 1000
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
