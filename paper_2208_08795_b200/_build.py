@@ -27,7 +27,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SRCS = ["full_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "morton_kernels.cu",
-           "morton_tmem_kernels.cu",
+           "morton_tmem_kernels.cu", "stream_kernels.cu",
            "sample_dispatch.cu",
            "sort_kernels.cu", "metrics_kernels.cu"]
 CXX_SRCS = ["capi.cpp", "pcs_api.cpp", "io.cpp"]

@@ -16,6 +16,8 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   // PCS_SAMPLER=rows forces the pruned-row engine (benchmarking / tests)
   const char* force = std::getenv("PCS_SAMPLER");
   const bool rows = force && std::string(force) == "rows";
+  // PCS_SAMPLER=stream forces the streaming engine (tests)
+  if (force && std::string(force) == "stream") return run_stream_any(p, nmax_sector, st);
   // full-window sectors: Morton rows beyond the register kernels' sweet
   // spot (PCS_MORTON=0 selects the storage-order rows, for A/B and tests;
   // PCS_MORTON_MIN moves the crossover)
@@ -37,9 +39,11 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
     e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && use_morton) e = morton_any();
   if (e == cudaErrorNotSupported) e = run_rows_any(p, nmax_sector, windowed, st);
+  // beyond every on-chip engine: d[] in global memory (L2), one cooperative
+  // launch per sector
+  if (e == cudaErrorNotSupported && !rows) e = run_stream_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && msg)
-    *msg = "sector of " + std::to_string(nmax_sector) +
-           " points exceeds the on-chip samplers of this build";
+    *msg = "sector of " + std::to_string(nmax_sector) + " points: no sampler of this build fits";
   return e;
 }
 

@@ -239,7 +239,10 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     sectored = method in ("afps", "npdu_afps")
     nmax = -(-n // (m if sectored else 1))
     windowed = method in ("npdu_fps", "npdu_afps") and k is not None and k < 2 * nmax - 1
-    rows = (env if env is not None else os.environ.get("PCS_SAMPLER")) == "rows"
+    forced = env if env is not None else os.environ.get("PCS_SAMPLER")
+    if forced == "stream":
+        return "stream_sector_kernel"
+    rows = forced == "rows"
     morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
               and _morton_fits(nmax, dtype))
     if morton and (rows or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
@@ -253,8 +256,14 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
         if nmax <= 4096 and (k + 62) // 32 <= 5 and dtype != "float64" and \
                 os.environ.get("PCS_NPDU_TMEM", "1") != "0":
             return "npdu_tmem_kernel"
-        return "npdu_warp_kernel" if nmax <= 8192 else "rows_kernel"
-    return "fps_full_kernel"
+        if nmax <= 8192:
+            return "npdu_warp_kernel"
+    elif nmax <= 3072:
+        return "fps_full_kernel"
+    # storage-order rows (one CTA or a cluster of <= 16 CTAs), else streaming
+    per_pt = 8 + 3 * (8 if dtype == "float64" else 4)
+    rows_cap = 16 * ((227 * 1024 - 4096) // per_pt // 32 - 2) * 32
+    return "rows_kernel" if nmax <= rows_cap else "stream_sector_kernel"
 
 
 def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,

@@ -392,19 +392,55 @@ def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
             np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
-def test_sector_beyond_on_chip_engines_is_an_error():
-    """No host fallback: a full-window sector larger than every on-chip
-    engine holds is reported, not sampled on the CPU."""
+def test_streaming_engine_beyond_on_chip_sectors(oracle):
+    """Sectors larger than every on-chip engine (d[] in global memory, one
+    cooperative launch per sector, grid barrier per iteration): FPS and NPDU
+    on a 300K-point cloud against the oracle."""
     import torch
 
     from paper_2208_08795_b200 import sample
 
-    xyz = torch.from_numpy(synth.uniform_cube(1, 300000, 3)).cuda()
-    with pytest.raises((RuntimeError, ValueError), match="exceeds the on-chip samplers"):
-        sample(xyz, 1000, method="fps")
-    # the same cloud as 4 AFPS sectors is fine
-    idx, st = sample(xyz, 1000, method="afps", m=4)
-    assert len(np.unique(idx.cpu().numpy())) == 1000
+    xyz = synth.uniform_cube(1, 300000, 3)
+    dev = torch.from_numpy(xyz).cuda()
+    for meth, c, k, first in (("fps", 600, None, "random"), ("npdu_fps", 1500, 129, "fixed")):
+        idx, st = sample(dev, c, method=meth, k=k, first=first, seed=5)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, 1, k or 0, first, 5)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=meth)
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
+@pytest.mark.parametrize("meth,n,c,m,k", [("fps", 3000, 2990, 1, 0), ("afps", 5000, 900, 3, 0),
+                                          ("npdu_afps", 4099, 1200, 2, 65)])
+def test_streaming_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k):
+    """The streaming engine forced onto small sectors (PCS_SAMPLER=stream):
+    coincident points drive the all-zero slow path; fp64 drop-in too."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    monkeypatch.setenv("PCS_SAMPLER", "stream")
+    xyz = synth.uniform_cube(2, n, 9)
+    xyz[1, : n // 2] = xyz[1, 0]
+    for first in ("fixed", "random"):
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method=meth, m=m, k=k or None,
+                         first=first, seed=3)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k, first, 3)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+    pts = synth.random_cloud(3001, 4)
+    got = _core_sample(meth, pts, c, m, k)
+    want = oracle.sample(meth, pts, c, m, k)
+    _same(got, *want)
+
+
+def _core_sample(meth, pts, c, m, k):
+    import paper_2208_08795_b200 as pcs
+
+    if meth == "fps":
+        return pcs.fps(pts, c, first="fixed")
+    if meth == "afps":
+        return pcs.afps(pts, c, m, first="fixed")
+    return pcs.npdu_afps(pts, c, m, k, first="fixed")
 
 
 def test_host_pipelined_path_matches_device_path():
