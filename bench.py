@@ -130,14 +130,15 @@ class ClockSampler:
 
 
 def ncu_traffic(workload):
-    """DRAM bytes per launch of the sampler kernel from the committed ncu
-    --set full summary for this workload (profiles/ncu_traffic.json)."""
+    """DRAM bytes per launch of the sampler kernel (and its issue rate) from
+    the committed ncu --set full summary for this workload
+    (profiles/ncu_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)[workload]
-        return float(d["dram_bytes"]), d["source"]
+        return float(d["dram_bytes"]), d["source"], d.get("ipc_per_sm")
     except (OSError, KeyError, ValueError):
-        return None, "no ncu capture for this workload"
+        return None, "no ncu capture for this workload", None
 
 
 def fp64_peak():
@@ -323,10 +324,14 @@ def main():
     peak, peak_src = fp64_peak()
     flops = 8.0 * evals_per_step
     achieved = flops / (kern_ms * 1e-3) / 1e12
-    traffic, traffic_src = ncu_traffic(args.workload)
+    traffic, traffic_src, ipc = ncu_traffic(args.workload)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if peak else None, "traffic": traffic,
                 "traffic_source": traffic_src,
+                # what actually limits the serial update->argmax->pivot chain:
+                # issued instructions per SM-cycle (ncu) against the 4 schedulers
+                "issue": ({"ipc_per_sm": ipc, "peak_ipc": 4.0, "frac": ipc / 4.0}
+                          if ipc else None),
                 "algorithmic_hbm_bytes": B * N * 12 + B * C * 4,
                 "kernel": pcs.kernel_family(w["method"], N, w["M"], w["K"]),
                 "kernel_ms": kern_ms, "algorithmic_flops": flops, "peak_source": peak_src,
