@@ -443,6 +443,24 @@ def _core_sample(meth, pts, c, m, k):
     return pcs.npdu_afps(pts, c, m, k, first="fixed")
 
 
+@pytest.mark.parametrize("meth,B,n,c,m,k", [
+    ("fps", 3, 1, 1, 1, 0), ("afps", 2, 5, 5, 5, 0), ("npdu_afps", 2, 7, 7, 7, 1),
+    ("npdu_fps", 2, 40, 40, 1, 1), ("npdu_fps", 2, 40, 17, 1, 1000), ("afps", 5000, 2, 2, 1, 0),
+    ("npdu_afps", 300, 96, 33, 3, 3), ("fps", 2, 4096, 1, 1, 0), ("afps", 1, 3073, 3073, 1, 0)])
+def test_edge_shapes(oracle, meth, B, n, c, m, k):
+    """Degenerate shapes: one point, quota 1, every point sampled, window 1,
+    window wider than the sector, thousands of two-point clouds."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    xyz = synth.uniform_cube(B, n, n + B)
+    idx, st = sample(torch.from_numpy(xyz).cuda(), c, method=meth, m=m, k=k or None)
+    want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k)
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+    np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
