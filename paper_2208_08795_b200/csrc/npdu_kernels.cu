@@ -449,7 +449,6 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     int* out32 = static_cast<int*>(p.out_idx) + out_base;
     long long* out64 = static_cast<long long*>(p.out_idx) + out_base;
     const bool idx64 = p.idx64 != 0;
-    double* const trace = p.trace;
     // output indices are buffered one per lane (sample t in lane t % 32) and
     // stored 32 at a time; the sampled bitmap is only needed by the
     // all-zero slow path, which folds the outputs into it on demand
@@ -486,31 +485,21 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
         dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
                         static_cast<double>(zs[jc]), px, py, pz);
       }
+      unsigned wmask = 0;
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
         const int j = j0 + 32 * q;
         const bool lower = j >= wb && j < we && dist[q] <= dj[q];
-        writes += lower ? 1u : 0u;
+        wmask |= lower ? (1u << q) : 0u;
         dj[q] = lower ? dist[q] : dj[q];
       }
+      writes += __popc(wmask);
       tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
         uint32_t hi, lo, jj;
         row_key(dj[q], r_lo + q, hi, lo, jj);
         store_row<RPL>(r_lo + q, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
-      }
-      if (trace) {
-        tm_wait_st();
-        for (int r = 0; r < rows; ++r) {
-          uint32_t t[2];
-          tm_ld(tm + 2 * r, t);
-          tm_wait_ld();
-          const int j = (r << 5) + lane;
-          if (j < n)
-            trace[static_cast<long long>(it - 1) * n + j] =
-                __hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0]));
-        }
       }
       uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
 #pragma unroll
@@ -594,7 +583,9 @@ cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
   const char* tmv = std::getenv("PCS_NPDU_TMEM");
   const bool use_tmem = !(tmv && tmv[0] == '0');
   const long long rows_needed = (p.K + 62) / 32;
-  if (use_tmem && !p.f64 && n <= 4096 && rows_needed <= 5) {
+  // (the TMEM kernel serves fp32 batches; distance traces come from the
+  // fp64 drop-in and take the shared-memory kernels)
+  if (use_tmem && !p.f64 && !p.trace && n <= 4096 && rows_needed <= 5) {
     auto by_cap = [&](auto rmax_tag) {
       constexpr int R = decltype(rmax_tag)::value;
       if (n <= 256) return run_npdu_tmem<R, 256>(p, st);
