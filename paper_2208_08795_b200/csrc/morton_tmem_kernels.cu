@@ -292,14 +292,6 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       if (lane == la) rmh = ha;
     }
     tm_wait_st();
-    if (p.trace) {
-      for (int l = 0; l < rpw; ++l) {
-        double dv;
-        uint32_t o;
-        tm_row_ld(tm + 4 * l, dv, o);
-        if (o != kNoIndex) p.trace[static_cast<long long>(it - 1) * n + o] = dv;
-      }
-    }
     TPROF_T(t1);
     // warp argmax: rows with the largest high word, exact key from TMEM
     uint32_t hi = __reduce_max_sync(kFull, rmh), lo = 0u, j = kNoIndex, pos = 0u;
@@ -505,7 +497,8 @@ cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
 
 // Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory).
 cudaError_t run_morton_tmem_any(SampleParams p, long long n, cudaStream_t st) {
-  if (p.f64) return cudaErrorNotSupported;
+  // fp32 batches; distance traces come from the fp64 drop-in (other engines)
+  if (p.f64 || p.trace) return cudaErrorNotSupported;
   const long long srows = (n + 31) / 32;
   for (int CS = 1; CS <= 16; CS *= 2) {
     const int rows = static_cast<int>((srows + CS - 1) / CS);
