@@ -333,7 +333,7 @@ def main():
                 "issue": ({"ipc_per_sm": ipc, "peak_ipc": 4.0, "frac": ipc / 4.0}
                           if ipc else None),
                 "algorithmic_hbm_bytes": B * N * 12 + B * C * 4,
-                "kernel": pcs.kernel_family(w["method"], N, w["M"], w["K"]),
+                "kernel": pcs.kernel_family(w["method"], N, w["M"], w["K"], batch=B),
                 "kernel_ms": kern_ms, "algorithmic_flops": flops, "peak_source": peak_src,
                 "note": "FP64 flops = 8 x dist_evals (3 sub, 3 mul, 2 add; no FMA); the "
                         "argmax work is not counted"}

@@ -5,10 +5,16 @@
 
 namespace pcsk {
 
-// Full-window sectors above this size take the Morton-row engine first; the
-// register-resident full kernel wins below it (r01 sweep: cfg5 FPS 2K full
-// 0.43 ms vs Morton 0.73 ms; 4K full 1.70 ms vs Morton 1.50 ms).
+// Full-window sectors above kMortonMin take the Morton-row engine first; the
+// register-resident full kernel wins below it when the SMs hold few sectors
+// (r01: cfg5 FPS 256 x 2K full 0.37 ms vs Morton 0.58 ms; 256 x 4K full 1.70
+// vs Morton 1.24 ms). With many sectors (>= 4 per SM) of more than 1024
+// points the Morton TMEM form wins already (its CTAs are small: 8 sectors
+// of 2K per SM against 2 for the register kernel): AFPS M=16 at 32K 5.13 ->
+// 3.18 ms, M=4 at 8K 1.33 -> 1.03 ms.
 constexpr long long kMortonMin = 3072;
+constexpr long long kMortonMinBusy = 1024;
+constexpr long long kBusySectors = 4 * 148;
 
 cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
                      std::string* msg) {
@@ -33,8 +39,9 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
     cudaError_t r = morton_tmem ? run_morton_tmem_any(p, nmax_sector, st) : cudaErrorNotSupported;
     return r == cudaErrorNotSupported ? run_morton_any(p, nmax_sector, st) : r;
   };
+  const bool busy = p.B * p.M >= kBusySectors && nmax_sector > kMortonMinBusy && !mmin;
   cudaError_t e = cudaErrorNotSupported;
-  if (use_morton && (rows || nmax_sector > morton_min)) e = morton_any();
+  if (use_morton && (rows || nmax_sector > morton_min || (busy && morton_tmem))) e = morton_any();
   if (e == cudaErrorNotSupported && !rows)
     e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && use_morton) e = morton_any();

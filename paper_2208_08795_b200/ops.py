@@ -228,7 +228,7 @@ def _morton_tmem_fits(n: int) -> bool:
 
 
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
-                  env: Optional[str] = None, dtype: str = "float32") -> str:
+                  env: Optional[str] = None, dtype: str = "float32", batch: int = 1) -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
     the per-sector register kernel for full windows up to 3072 points, the
     Morton-row engine for larger full windows (one CTA or a cluster), the
@@ -245,11 +245,14 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     rows = forced == "rows"
     morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
               and _morton_fits(nmax, dtype))
-    if morton and (rows or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
-        if dtype != "float64" and os.environ.get("PCS_MORTON_TMEM", "1") != "0" and \
-                _morton_tmem_fits(nmax):
-            return "morton_tmem_kernel"
-        return "morton_rows_kernel"
+    tmem = dtype != "float64" and os.environ.get("PCS_MORTON_TMEM", "1") != "0" and \
+        _morton_tmem_fits(nmax)
+    # many sectors (>= 4 per SM) of more than 1024 points: the TMEM form
+    # already wins (csrc/sample_dispatch.cu, kMortonMinBusy)
+    busy = (batch * (m if sectored else 1) >= 4 * 148 and nmax > 1024 and tmem
+            and "PCS_MORTON_MIN" not in os.environ)
+    if morton and (rows or busy or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
+        return "morton_tmem_kernel" if tmem else "morton_rows_kernel"
     if rows:
         return "rows_kernel"
     if windowed:

@@ -461,6 +461,23 @@ def test_edge_shapes(oracle, meth, B, n, c, m, k):
     np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+def test_busy_afps_takes_morton_engine(oracle):
+    """Many (>= 4 per SM) full-window sectors of 1025-3072 points take the
+    TMEM Morton engine (small CTAs, many per SM); bit-exact with the oracle."""
+    import torch
+
+    import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import sample
+
+    B, n, m, c = 150, 4400, 4, 1000
+    assert pcs.kernel_family("afps", n, m, batch=B) == "morton_tmem_kernel"
+    xyz = synth.stable_sort_np(synth.primitives(B, n, 5, seed=12), 0)[0]
+    idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="afps", m=m, first="random", seed=2)
+    want_idx, want_st = oracle.sample_batch_f32("afps", xyz, c, m, 0, "random", 2)
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+    np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
