@@ -184,6 +184,11 @@ __global__ void __launch_bounds__(kSortThreads)
 // CS > 1: the cloud spans a cluster of CS CTAs (global word index
 // rank * NP + local); steps whose partner lives in another CTA (j >= NP) go
 // through DSMEM with cluster barriers.
+// shared-memory word index with one pad word per 32: the blocked register
+// layout (thread t's words t*E .. t*E+E-1) would otherwise put all 32 lanes
+// of a warp on the same banks when it spills to / reloads from shared memory
+__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
+
 template <int E, int CS>
 __global__ void __launch_bounds__(kSortThreads)
     bitonic_reg_kernel(const float* __restrict__ xyz, long long N, int axis,
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kSortThreads)
     long long j = k >> 1;
     if (j >= 32 * E) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) words[t * E + e] = x[e];
+      for (int e = 0; e < E; ++e) words[spad(t * E + e)] = x[e];
       if constexpr (CS > 1) {
         if (j >= NP) {
           // cross-CTA steps: the lower CTA of each pair exchanges in place
@@ -243,10 +248,10 @@ __global__ void __launch_bounds__(kSortThreads)
             if (rank < partner) {
               unsigned long long* remote = cg::this_cluster().map_shared_rank(words, partner);
               for (int q = t; q < NP; q += kSortThreads) {
-                const unsigned long long a = words[q], c = remote[q];
+                const unsigned long long a = words[spad(q)], c = remote[spad(q)];
                 if ((a > c) == (((base + q) & k) == 0)) {
-                  words[q] = c;
-                  remote[q] = a;
+                  words[spad(q)] = c;
+                  remote[spad(q)] = a;
                 }
               }
             }
@@ -259,16 +264,16 @@ __global__ void __launch_bounds__(kSortThreads)
         const int lj = __ffsll(j) - 1;
         for (int q = t; q < NP / 2; q += kSortThreads) {
           const int lo = ((q >> lj) << (lj + 1)) | (q & static_cast<int>(j - 1)), hi = lo + static_cast<int>(j);
-          const unsigned long long a = words[lo], c = words[hi];
+          const unsigned long long a = words[spad(lo)], c = words[spad(hi)];
           if ((a > c) == (((base + lo) & k) == 0)) {
-            words[lo] = c;
-            words[hi] = a;
+            words[spad(lo)] = c;
+            words[spad(hi)] = a;
           }
         }
         __syncthreads();
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = words[t * E + e];
+      for (int e = 0; e < E; ++e) x[e] = words[spad(t * E + e)];
       __syncthreads();
     }
     for (; j >= E; j >>= 1) {
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kSortThreads)
 template <int E, int CS = 1>
 cudaError_t launch_reg_sort(const float* xyz, long long batch, long long n, int axis,
                             float* out_xyz, int* out_perm, cudaStream_t st) {
-  const size_t smem = sizeof(unsigned long long) * E * kSortThreads;
+  const size_t smem = sizeof(unsigned long long) * (E * kSortThreads + E * kSortThreads / 32);
   auto kern = bitonic_reg_kernel<E, CS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
