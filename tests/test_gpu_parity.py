@@ -478,6 +478,44 @@ def test_busy_afps_takes_morton_engine(oracle):
     np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("meth,n,c,m,k", [("afps", 1 << 20, 1 << 18, 1024, None),
+                                          ("npdu_afps", 65536, 8192, 64, 65),
+                                          ("afps", 100003, 9001, 37, None)])
+def test_sector_shards_reassemble_on_device(meth, n, c, m, k):
+    """The multi-GPU sector split (shard.sector_shard + index_base /
+    sector_base) run shard by shard on one device: the concatenated shards
+    equal the whole-cloud call bit for bit -- indices, sector ids and the
+    per-sector random starts (seed ^ global sector)."""
+    import torch
+
+    from paper_2208_08795_b200 import sample, shard
+
+    xyz = torch.from_numpy(synth.uniform_cube(1, n, 17)).cuda()
+    xs = sample(xyz, c, method=meth, m=m, k=k, sort="x", first="random", seed=9,
+                return_sector=True)
+    whole_idx, whole_st, whole_sec = xs[0], xs[1], xs[2]
+    srt = pcs_sort(xyz)
+    for world in (2, 3, 8):
+        parts_i, parts_s, st = [], [], torch.zeros(4, dtype=torch.int64, device="cuda")
+        for rank in range(world):
+            sh = shard.sector_shard(n, c, m, world, rank)
+            i, s_, sec = sample(srt[:, sh.point_lo:sh.point_hi], sh.c, method=meth, m=sh.m, k=k,
+                                first="random", seed=9, return_sector=True,
+                                index_base=sh.point_lo, sector_base=sh.sector_lo)
+            parts_i.append(i)
+            parts_s.append(sec)
+            st += s_[0]
+        assert torch.equal(torch.cat(parts_i, 1), whole_idx), world
+        assert torch.equal(torch.cat(parts_s, 1), whole_sec), world
+        assert torch.equal(st, whole_st[0]), world
+
+
+def pcs_sort(xyz):
+    from paper_2208_08795_b200 import sort_axis
+
+    return sort_axis(xyz, "x")[0]
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
