@@ -16,6 +16,7 @@
 // by their owner (row r -> warp r % W), as in the shared-memory engine.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -484,13 +485,28 @@ cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Warps per CTA: the fewest that give one row per lane, except that CTAs
+// of 65-128 rows get 8 warps when the SMs hold about two sectors or fewer
+// (r01: 256 x 4K FPS 1.24 -> 1.13 ms; with ~7 sectors per SM the smaller
+// CTAs win: AFPS M=4 at 8K 1.09 vs 1.37 ms). PCS_MORTON_TMEM_W overrides.
+int morton_tmem_w(int rows, long long sectors) {
+  int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
+  if (w == 4 && rows > 64 && sectors <= 2 * 148) w = 8;
+  if (const char* e = std::getenv("PCS_MORTON_TMEM_W")) {
+    const int v = std::atoi(e);
+    if (v == 4 || v == 8 || v == 16) w = std::max(w, v);
+  }
+  return w;
+}
+
 template <int CS>
 cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
   // one row per lane: W >= rows / 32, a multiple of 4 (whole lane quarters)
-  if (rows <= 128) return launch_morton_tmem<4, CS>(p, rows, st);
-  if (rows <= 256) return launch_morton_tmem<8, CS>(p, rows, st);
-  if (rows <= 512) return launch_morton_tmem<16, CS>(p, rows, st);
-  return cudaErrorNotSupported;
+  const int w = morton_tmem_w(rows, p.B * p.M);
+  if (rows > 512) return cudaErrorNotSupported;
+  if (w <= 4) return launch_morton_tmem<4, CS>(p, rows, st);
+  if (w <= 8) return launch_morton_tmem<8, CS>(p, rows, st);
+  return launch_morton_tmem<16, CS>(p, rows, st);
 }
 
 }  // namespace
@@ -503,7 +519,7 @@ cudaError_t run_morton_tmem_any(SampleParams p, long long n, cudaStream_t st) {
   for (int CS = 1; CS <= 16; CS *= 2) {
     const int rows = static_cast<int>((srows + CS - 1) / CS);
     if (rows > 512) continue;
-    const int W = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
+    const int W = morton_tmem_w(rows, p.B * p.M);
     const int rpw = (rows + W - 1) / W;
     if (morton_tmem_smem(rpw * W * 32, W, CS) > kMaxSmem) continue;
     switch (CS) {

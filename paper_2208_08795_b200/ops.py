@@ -217,7 +217,7 @@ def _morton_tmem_fits(n: int) -> bool:
         rows = -(-srows // cs)
         if rows > 512:
             continue
-        w = 4 if rows <= 128 else 8 if rows <= 256 else 16
+        w = 8 if rows <= 256 else 16  # largest W the dispatcher may pick (smem check)
         np_ = -(-rows // w) * w * 32
         nbytes = np_ * 12 + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
         nbytes += 2 * cs * w * 48 if cs > 1 else 0
