@@ -506,7 +506,7 @@ cudaError_t launch_morton(SampleParams p, int np, cudaStream_t st) {
 int morton_w(int rows) {
   int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
   if (const char* e = std::getenv("PCS_MORTON_W")) w = std::max(w, std::atoi(e));
-  return w > 16 ? 32 : w;
+  return w > 8 ? 16 : w;
 }
 
 template <typename CT, int CS>
@@ -518,8 +518,7 @@ cudaError_t launch_morton_w(SampleParams p, int chunk, cudaStream_t st) {
   switch (w) {
     case 4: return launch_morton<CT, 4, CS>(p, np, st);
     case 8: return launch_morton<CT, 8, CS>(p, np, st);
-    case 16: return launch_morton<CT, 16, CS>(p, np, st);
-    default: return launch_morton<CT, 32, CS>(p, np, st);
+    default: return launch_morton<CT, 16, CS>(p, np, st);
   }
 }
 
