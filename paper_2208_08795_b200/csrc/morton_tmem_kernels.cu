@@ -52,7 +52,10 @@ __device__ __forceinline__ void tm_row_ld(uint32_t a, double& d, uint32_t& orig)
 // row r belongs to warp r % W as its row l = r / W, stored at TMEM columns
 // tm + 4l .. 4l+3 of the warp's quarter. One row per lane for the row
 // metadata (box, max high word), as in the shared-memory engine.
-template <int W, int CS>
+// WIN (NPDU variants, update_window, proj/src/sectors.cpp:53-61): slots
+// keep storage order (windows are storage ranges) and only rows meeting the
+// window are candidates; the rest of the engine is unchanged.
+template <int W, int CS, bool WIN>
 __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams p, int tm_cols) {
   static_assert(W % 4 == 0, "whole lane quarters");
   extern __shared__ __align__(16) unsigned char smem[];
@@ -120,7 +123,12 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   __syncthreads();
   // ---- 2. Morton keys (code << 32 | storage slot) over the xs/ys region
   unsigned long long* key = reinterpret_cast<unsigned long long*>(xs);
-  {
+  if constexpr (WIN) {
+    for (int jl = threadIdx.x; jl < np; jl += T) {
+      const int gj = to_sector(jl);
+      key[jl] = ((jl >> 5) < srows_local && gj < n) ? static_cast<unsigned long long>(jl) : ~0ull;
+    }
+  } else {
     const float bx0 = ord2f(scratch[0]), by0 = ord2f(scratch[2]), bz0 = ord2f(scratch[4]);
     const float ext = fmaxf(fmaxf(ord2f(scratch[1]) - bx0, ord2f(scratch[3]) - by0),
                             ord2f(scratch[5]) - bz0);
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   }
   __syncthreads();
   // ---- 3. bitonic sort (non-power-of-two size: mirrored first merge step)
-  for (int kk = 2; kk < 2 * np; kk <<= 1) {
+  for (int kk = 2; kk < (WIN ? 0 : 2 * np); kk <<= 1) {
     for (int jj = kk >> 1; jj > 0; jj >>= 1) {
       const int mask = jj == (kk >> 1) ? kk - 1 : jj;
       for (int i = threadIdx.x; i < np; i += T) {
@@ -242,11 +250,24 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
+  const long long K = p.K;
+  const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
+  unsigned long long evals = 0;
   auto iterate = [&](auto f2f_tag) {
   constexpr bool F2F = decltype(f2f_tag)::value;
   for (int it = 1; it < g.quota; ++it) {
     TPROF_T(t0);
+    [[maybe_unused]] int wb = 0, we = n;
+    if constexpr (WIN) {
+      wb = cur >= half_down ? cur - half_down : 0;
+      we = min(n, cur + half_up);
+      evals += static_cast<unsigned long long>(we - wb);
+    }
     bool need = r < rows;
+    if constexpr (WIN) {
+      const int R = r * CS + rank;  // this lane's row in sector order
+      need = need && (R << 5) < we && (R << 5) + 32 > wb;
+    }
     if (need) {
       const float lb = __fadd_rd(__fadd_rd(gap2(bx0, bx1, pfx, pfx), gap2(by0, by1, pfy, pfy)),
                                  gap2(bz0, bz1, pfz, pfz));
@@ -276,8 +297,12 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       tm_wait_ld();
       double da = __hiloint2double(static_cast<int>(ra4[1]), static_cast<int>(ra4[0]));
       double db = __hiloint2double(static_cast<int>(rb4[1]), static_cast<int>(rb4[0]));
-      const bool wa = ra4[2] != kNoIndex && ea <= da;
-      const bool wbb = lb2 != la && rb4[2] != kNoIndex && eb <= db;
+      bool wa = ra4[2] != kNoIndex && ea <= da;
+      bool wbb = lb2 != la && rb4[2] != kNoIndex && eb <= db;
+      if constexpr (WIN) {
+        wa = wa && static_cast<int>(ra4[2]) >= wb && static_cast<int>(ra4[2]) < we;
+        wbb = wbb && static_cast<int>(rb4[2]) >= wb && static_cast<int>(rb4[2]) < we;
+      }
       writes += (wa ? 1u : 0u) + (wbb ? 1u : 0u);
       da = wa ? ea : da;
       db = lb2 == la ? da : (wbb ? eb : db);
@@ -427,7 +452,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
     if (lane == 0 && ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
     if (rank == 0 && threadIdx.x == 0) {
       const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
-      atomicAdd(st + 0, iters * static_cast<unsigned long long>(n));
+      atomicAdd(st + 0, WIN ? evals : iters * static_cast<unsigned long long>(n));
       atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
       atomicAdd(st + 3, iters);
     }
@@ -450,7 +475,7 @@ size_t morton_tmem_smem(int np, int W, int CS) {
   return bytes;
 }
 
-template <int W, int CS>
+template <int W, int CS, bool WIN>
 cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
   const int rpw = (rows + W - 1) / W;
   const int np = rpw * W * 32;
@@ -460,7 +485,7 @@ cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
   int cols = 32;
   while (cols < W * rpw) cols *= 2;  // W/4 warps per quarter x 4 columns x rpw rows
   if (cols > 512) return cudaErrorNotSupported;
-  auto kern = morton_tmem_kernel<W, CS>;
+  auto kern = morton_tmem_kernel<W, CS, WIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -504,9 +529,14 @@ cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
   // one row per lane: W >= rows / 32, a multiple of 4 (whole lane quarters)
   const int w = morton_tmem_w(rows, p.B * p.M);
   if (rows > 512) return cudaErrorNotSupported;
-  if (w <= 4) return launch_morton_tmem<4, CS>(p, rows, st);
-  if (w <= 8) return launch_morton_tmem<8, CS>(p, rows, st);
-  return launch_morton_tmem<16, CS>(p, rows, st);
+  if (p.K > 0) {
+    if (w <= 4) return launch_morton_tmem<4, CS, true>(p, rows, st);
+    if (w <= 8) return launch_morton_tmem<8, CS, true>(p, rows, st);
+    return launch_morton_tmem<16, CS, true>(p, rows, st);
+  }
+  if (w <= 4) return launch_morton_tmem<4, CS, false>(p, rows, st);
+  if (w <= 8) return launch_morton_tmem<8, CS, false>(p, rows, st);
+  return launch_morton_tmem<16, CS, false>(p, rows, st);
 }
 
 }  // namespace

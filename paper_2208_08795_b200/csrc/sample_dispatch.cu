@@ -42,6 +42,13 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   const bool busy = p.B * p.M >= kBusySectors && nmax_sector > kMortonMinBusy && !mmin;
   cudaError_t e = cudaErrorNotSupported;
   if (use_morton && (rows || nmax_sector > morton_min || (busy && morton_tmem))) e = morton_any();
+  // windowed sectors past the TMEM NPDU kernel (> 4096 points, fp32): the
+  // TMEM row engine in storage order, rows restricted to the window
+  // (PCS_NPDU_BIG=0 keeps the warp / shared-memory row kernels)
+  const char* nb = std::getenv("PCS_NPDU_BIG");
+  if (e == cudaErrorNotSupported && !rows && windowed && !p.f64 && nmax_sector > 4096 &&
+      !(nb && std::string(nb) == "0"))
+    e = run_morton_tmem_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && !rows)
     e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && use_morton) e = morton_any();

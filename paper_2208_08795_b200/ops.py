@@ -259,6 +259,9 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
         if nmax <= 4096 and (k + 62) // 32 <= 5 and dtype != "float64" and \
                 os.environ.get("PCS_NPDU_TMEM", "1") != "0":
             return "npdu_tmem_kernel"
+        if nmax > 4096 and dtype != "float64" and os.environ.get("PCS_NPDU_BIG", "1") != "0" \
+                and _morton_tmem_fits(nmax):
+            return "morton_tmem_kernel"
         if nmax <= 8192:
             return "npdu_warp_kernel"
     elif nmax <= 3072:

@@ -516,6 +516,29 @@ def pcs_sort(xyz):
     return sort_axis(xyz, "x")[0]
 
 
+@pytest.mark.parametrize("n,c,m,k", [(8192, 2048, 1, 65), (20000, 3000, 1, 129), (40000, 4000, 1, 33),
+                                     (32768, 4096, 4, 65), (5000, 2500, 1, 7)])
+def test_npdu_big_sectors_tmem_rows(oracle, n, c, m, k):
+    """Windowed sectors past 4096 points (fp32): the TMEM row engine in
+    storage order with window-restricted rows (1 CTA or a cluster);
+    coincident points and random starts."""
+    import torch
+
+    import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import sample
+
+    meth = "npdu_afps" if m > 1 else "npdu_fps"
+    assert pcs.kernel_family(meth, n, m, k) == "morton_tmem_kernel"
+    xyz = synth.stable_sort_np(synth.uniform_cube(2, n, n), 0)[0]
+    xyz[1, 100:600] = xyz[1, 99]
+    for first in ("fixed", "random"):
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method=meth, m=m, k=k, first=first,
+                         seed=4)
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k, first, 4)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{n} {first}")
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_host_pipelined_path_matches_device_path():
     """CPU (pinned or not) input: chunked H2D/compute/D2H gives the same
     results as the device path."""
