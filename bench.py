@@ -344,11 +344,12 @@ def main():
         pinned = torch.from_numpy(xyz_host).pin_memory()
 
         def e2e_step():
-            # the public API with host buffers: pinned batch in, host results
-            # out (pipelined H2D / sort+sample / D2H inside the call)
+            # the C-ABI host-buffer entry (pcs_sample_host_batch, through
+            # pcs.sample_host_batch): pinned batch in, host results out,
+            # chunked H2D / sort + sample / D2H inside the native call
             if sh is None:
-                return pcs.sample(pinned, C, method=w["method"], m=w["M"], k=w["K"],
-                                  sort=w["sort"])
+                return pcs.sample_host_batch(pinned, C, method=w["method"], m=w["M"], k=w["K"],
+                                             sort=w["sort"])
             res = step(pinned.to(dev, non_blocking=True))
             return tuple(t.cpu() for t in res)
 
@@ -391,9 +392,12 @@ def main():
                "ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
                "h2d_gbps": pinned.numel() * pinned.element_size() / min(h2d) / 1e6,
                "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
-               "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in r)),
-               "path": "pcs.sample(pinned host tensor): chunked H2D overlapped with sort+sample, "
-                       "D2H of indices, stats (and perm when sorting)"}
+               "d2h_bytes_per_step": int(sum(t.nbytes if hasattr(t, "nbytes") else
+                                             t.numel() * t.element_size() for t in r)),
+               "path": ("C-ABI pcs_sample_host_batch (pinned host tensor in, host arrays out): "
+                        "chunked H2D overlapped with sort+sample, D2H of indices, stats (and "
+                        "perm when sorting)") if sh is None else
+                       "pinned H2D, sort, sample of this rank's sectors, D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

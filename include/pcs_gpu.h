@@ -25,6 +25,8 @@
  *                           the four samplers (no reference equivalent: the
  *                           reference is per-cloud only)
  *   pcs_gpu_sort_axis    <- batched device form of exact_sort
+ *   pcs_sample_host_batch <- the per-cloud samplers called over a batch of
+ *                           host clouds (+ exact_sort), in one pipelined call
  *
  * Semantics are the reference's, bit for bit: indices, sector_of and the
  * OpStats counters (include/pcs/op_stats.hpp:10-25) equal the reference CPU
@@ -118,6 +120,20 @@ int pcs_gpu_sort_axis(int32_t coord_dtype, const void* xyz, int64_t batch, int64
 int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int64_t m,
                     int64_t k, int32_t seed_policy, uint64_t seed, uint32_t threads,
                     int64_t* out_indices, int64_t* out_sector, uint64_t* out_stats);
+
+/* Host-buffer batch: the reference's per-cloud samplers over B clouds in one
+ * call (what a caller of pcs::npdu_afps & co. does in a loop over its
+ * clouds). Same fields as pcs_gpu_args, but xyz, out_indices, out_sector and
+ * out_stats are HOST pointers (seeds, when given, too). The batch streams
+ * through the device in `chunks` pieces (<= 0: a default): the copy of
+ * piece i+1 overlaps the axis sort + sampling of piece i, results return
+ * as pieces complete. sort_axis -1: no sort; 0/1/2: the clouds are first
+ * stably sorted along x/y/z (exact_sort) and indices refer to the sorted
+ * clouds; out_perm (host int32 (B, N), optional) receives the sort
+ * permutation. Pinned host memory gives the overlap; pageable memory works.
+ * Synchronous. */
+int pcs_sample_host_batch(const pcs_gpu_args* host_args, int32_t sort_axis, int32_t* out_perm,
+                          int32_t chunks);
 
 /* detail::local_fps over one storage range [sector_begin, sector_end) of a
  * cloud. k < 0 means no window (std::nullopt); k == 0 is rejected exactly as

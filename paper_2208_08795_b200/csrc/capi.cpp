@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "internal.h"
@@ -201,6 +202,123 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   return rc;
+}
+
+int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
+                          int32_t chunks) {
+  clear_error();
+  if (!ha) { set_error("pcs_sample_host_batch: null args"); return PCS_ERR_INVALID_ARGUMENT; }
+  std::string msg;
+  int rc = validate_sample(ha->method, ha->n, ha->c, ha->m, ha->k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  if (ha->batch < 0) { set_error("pcs_sample_host_batch: batch must be >= 0"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (sort_axis < -1 || sort_axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
+  const int64_t B = ha->batch, N = ha->n, C = ha->c;
+  if (B == 0) return PCS_OK;
+  if (!ha->xyz || !ha->out_indices) { set_error("pcs_sample_host_batch: null buffer"); return PCS_ERR_INVALID_ARGUMENT; }
+  const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
+  const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
+  const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
+  int nch = chunks > 0 ? chunks : 8;
+  if (nch > B) nch = static_cast<int>(B);
+  // one copy stream + kWorkers compute streams per device, created once and
+  // kept (stream creation costs more than a small batch's sampling); calls
+  // on the same device are serialised
+  constexpr int kWorkers = 4, kEvents = 64;
+  struct DevStreams {
+    cudaStream_t copy = nullptr, work[kWorkers] = {};
+    cudaEvent_t ev[kEvents] = {};
+    bool ok = false;
+  };
+  static std::mutex mu;
+  static DevStreams per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev >= 64) { set_error("pcs_sample_host_batch: device ordinal >= 64"); return PCS_ERR_UNSUPPORTED; }
+  std::lock_guard<std::mutex> lock(mu);
+  DevStreams& ds = per_dev[dev];
+  if (!ds.ok) {
+    e = cudaStreamCreateWithFlags(&ds.copy, cudaStreamNonBlocking);
+    for (int w = 0; w < kWorkers && e == cudaSuccess; ++w)
+      e = cudaStreamCreateWithFlags(&ds.work[w], cudaStreamNonBlocking);
+    for (int i = 0; i < kEvents && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&ds.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e);
+    ds.ok = true;
+  }
+  cudaStream_t copy = ds.copy;
+  cudaStream_t* work = ds.work;
+  if (nch > kEvents - 1) nch = kEvents - 1;
+  void* ws = nullptr;
+  size_t off_xyz = 0, off_srt = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
+  if (e == cudaSuccess) {
+    size_t bytes = 0;
+    auto take = [&](size_t& off, size_t len) { off = bytes; bytes += (len + 255) & ~size_t(255); };
+    take(off_xyz, cloud_bytes * B);
+    take(off_srt, sort_axis >= 0 ? cloud_bytes * B : 0);
+    take(off_perm, sort_axis >= 0 ? 4 * static_cast<size_t>(N) * B : 0);
+    take(off_idx, isize * static_cast<size_t>(C) * B);
+    take(off_sec, ha->out_sector ? 4 * static_cast<size_t>(C) * B : 0);
+    take(off_st, ha->out_stats ? 32 * static_cast<size_t>(B) : 0);
+    take(off_seed, ha->seeds ? 8 * static_cast<size_t>(B) : 0);
+    e = workspace_alloc(&ws, bytes, copy);
+  }
+  char* base = static_cast<char*>(ws);
+  if (e == cudaSuccess && ha->seeds)
+    e = cudaMemcpyAsync(base + off_seed, ha->seeds, 8 * B, cudaMemcpyHostToDevice, copy);
+  cudaEvent_t seeds_ready = ds.ev[kEvents - 1];  // the workspace (and seeds) exist
+  if (e == cudaSuccess) e = cudaEventRecord(seeds_ready, copy);
+  for (int i = 0; i < nch && e == cudaSuccess; ++i) {
+    const int64_t b0 = B * i / nch, b1 = B * (i + 1) / nch, nb = b1 - b0;
+    if (nb == 0) continue;
+    cudaStream_t w = work[i % kWorkers];
+    char* dx = base + off_xyz + cloud_bytes * b0;
+    e = cudaMemcpyAsync(dx, static_cast<const char*>(ha->xyz) + cloud_bytes * b0,
+                        cloud_bytes * nb, cudaMemcpyHostToDevice, copy);
+    cudaEvent_t ready = ds.ev[i];
+    if (e == cudaSuccess) e = cudaEventRecord(ready, copy);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(w, ready, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(w, seeds_ready, 0);
+    const void* src = dx;
+    int32_t* dperm = reinterpret_cast<int32_t*>(base + off_perm) + N * b0;
+    if (e == cudaSuccess && sort_axis >= 0) {
+      char* ds = base + off_srt + cloud_bytes * b0;
+      e = launch_sort(ha->coord_dtype, dx, nb, N, sort_axis, ds, dperm, w);
+      src = ds;
+    }
+    pcs_gpu_args a = *ha;
+    a.xyz = src;
+    a.batch = nb;
+    a.seeds = ha->seeds ? reinterpret_cast<const uint64_t*>(base + off_seed) + b0 : nullptr;
+    a.out_indices = base + off_idx + isize * C * b0;
+    a.out_sector = ha->out_sector ? reinterpret_cast<int32_t*>(base + off_sec) + C * b0 : nullptr;
+    a.out_stats = ha->out_stats ? reinterpret_cast<uint64_t*>(base + off_st) + 4 * b0 : nullptr;
+    if (e == cudaSuccess) {
+      e = launch_sample(a, w, &msg);
+      if (e != cudaSuccess) break;
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<char*>(ha->out_indices) + isize * C * b0, a.out_indices,
+                          isize * C * nb, cudaMemcpyDeviceToHost, w);
+    if (e == cudaSuccess && ha->out_sector)
+      e = cudaMemcpyAsync(ha->out_sector + C * b0, a.out_sector, 4 * C * nb, cudaMemcpyDeviceToHost, w);
+    if (e == cudaSuccess && ha->out_stats)
+      e = cudaMemcpyAsync(ha->out_stats + 4 * b0, a.out_stats, 32 * nb, cudaMemcpyDeviceToHost, w);
+    if (e == cudaSuccess && sort_axis >= 0 && out_perm)
+      e = cudaMemcpyAsync(out_perm + N * b0, dperm, 4 * N * nb, cudaMemcpyDeviceToHost, w);
+  }
+  for (int w = 0; w < kWorkers; ++w) {
+    const cudaError_t e2 = cudaStreamSynchronize(work[w]);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (ws) cudaFreeAsync(ws, copy);  // every use above has completed
+  {
+    const cudaError_t e2 = cudaStreamSynchronize(copy);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, msg);
+  return PCS_OK;
 }
 
 int pcs_local_fps_host(const double* xyz, int64_t n, int64_t sb, int64_t se, int64_t quota,

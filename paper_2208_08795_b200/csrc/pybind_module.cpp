@@ -259,6 +259,41 @@ PYBIND11_MODULE(_core, m) {
         py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
         py::arg("out_stats"), py::arg("stream"), py::arg("index_base") = 0,
         py::arg("sector_base") = 0);
+  // the host-buffer batch entry (pointers into host memory, e.g. pinned
+  // torch tensors); the GIL is released for the synchronous call
+  m.def("sample_host_ptr",
+        [](int method, int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n,
+           std::int64_t c, std::int64_t mm, std::int64_t k, int seed_policy, std::uint64_t seed,
+           std::uintptr_t seeds, int index_dtype, std::uintptr_t out_idx, std::uintptr_t out_sector,
+           std::uintptr_t out_stats, int sort_axis, std::uintptr_t out_perm, int chunks) {
+          pcs_gpu_args a{};
+          a.method = method;
+          a.coord_dtype = coord_dtype;
+          a.xyz = reinterpret_cast<const void*>(xyz);
+          a.batch = batch;
+          a.n = n;
+          a.c = c;
+          a.m = mm;
+          a.k = k;
+          a.seed_policy = seed_policy;
+          a.seed = seed;
+          a.seeds = reinterpret_cast<const std::uint64_t*>(seeds);
+          a.index_dtype = index_dtype;
+          a.out_indices = reinterpret_cast<void*>(out_idx);
+          a.out_sector = reinterpret_cast<std::int32_t*>(out_sector);
+          a.out_stats = reinterpret_cast<std::uint64_t*>(out_stats);
+          int rc;
+          {
+            py::gil_scoped_release nogil;
+            rc = pcs_sample_host_batch(&a, sort_axis, reinterpret_cast<std::int32_t*>(out_perm),
+                                       chunks);
+          }
+          check(rc);
+        },
+        py::arg("method"), py::arg("coord_dtype"), py::arg("xyz"), py::arg("batch"), py::arg("n"),
+        py::arg("c"), py::arg("m"), py::arg("k"), py::arg("seed_policy"), py::arg("seed"),
+        py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
+        py::arg("out_stats"), py::arg("sort_axis"), py::arg("out_perm"), py::arg("chunks") = 0);
   m.def("sort_device",
         [](int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n, int axis,
            std::uintptr_t out_xyz, std::uintptr_t out_perm, std::uintptr_t stream) {

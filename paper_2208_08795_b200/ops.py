@@ -272,12 +272,47 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     return "rows_kernel" if nmax <= rows_cap else "stream_sector_kernel"
 
 
-def sample_host_batch(xyz: np.ndarray, c: int, method: str = "afps", m: int = 1,
+def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
                       k: Optional[int] = None, first: str = "fixed", seed: int = 0,
-                      sort: Optional[str] = None, device: str = "cuda"):
-    """Host (numpy) batch in, host (numpy) results out; the pipelined host
-    path of :func:`sample`."""
-    host = torch.from_numpy(np.ascontiguousarray(xyz))
+                      sort: Optional[str] = None, device: str = "cuda",
+                      index_dtype=np.int32, return_sector: bool = False, chunks: int = 0):
+    """Host batch in, host results out, through the C-ABI host entry
+    ``pcs_sample_host_batch`` (include/pcs_gpu.h): the per-cloud samplers
+    over a batch in one native, pipelined call (H2D of a chunk overlaps the
+    sort + sampling of the previous one). ``xyz``: (B, N, 3) float32/float64
+    numpy array or CPU torch tensor (pin it -- ``tensor.pin_memory()`` -- for
+    copy/compute overlap). Returns numpy ``(indices (B, c), stats (B, 4))``
+    plus ``sector_of`` when ``return_sector`` and ``perm`` when ``sort``."""
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    if first not in ("fixed", "random"):
+        raise ValueError("first must be 'random' or 'fixed'")
+    x = xyz if isinstance(xyz, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(xyz))
+    if x.is_cuda:
+        raise ValueError("sample_host_batch takes host memory; use sample() for CUDA tensors")
+    x = x.unsqueeze(0) if x.dim() == 2 else x
+    if x.dim() != 3 or x.shape[-1] != 3 or x.dtype not in (torch.float32, torch.float64):
+        raise ValueError("expected a float32/float64 (B, N, 3) array")
+    x = x.contiguous()
+    B, N = x.shape[0], x.shape[1]
+    idx64 = np.dtype(index_dtype) == np.int64
+    pin = x.is_pinned()
+    idx = torch.empty((B, max(int(c), 0)), dtype=torch.int64 if idx64 else torch.int32,
+                      pin_memory=pin)
+    stats = torch.empty((B, 4), dtype=torch.int64, pin_memory=pin)
+    sec = torch.empty((B, max(int(c), 0)), dtype=torch.int32, pin_memory=pin) if return_sector else None
+    perm = torch.empty((B, N), dtype=torch.int32, pin_memory=pin) if sort else None
     with torch.cuda.device(torch.device(device)):
-        res = sample(host, c, method=method, m=m, k=k, first=first, seed=seed, sort=sort)
-    return tuple(t.numpy() for t in res)
+        _core.sample_host_ptr(METHODS[method], 1 if x.dtype == torch.float64 else 0,
+                              x.data_ptr(), B, N, int(c), int(m), int(k) if k is not None else 0,
+                              1 if first == "fixed" else 0, int(seed) & (2**64 - 1), 0,
+                              1 if idx64 else 0, idx.data_ptr(),
+                              sec.data_ptr() if sec is not None else 0, stats.data_ptr(),
+                              _AXES[sort] if sort is not None else -1,
+                              perm.data_ptr() if perm is not None else 0, int(chunks))
+    out = [idx.numpy(), stats.numpy()]
+    if return_sector:
+        out.append(sec.numpy())
+    if perm is not None:
+        out.append(perm.numpy())
+    return tuple(out)

@@ -556,6 +556,20 @@ def test_host_pipelined_path_matches_device_path():
         np.testing.assert_array_equal(a.cpu().numpy(), b.numpy())
     npi = sample_host_batch(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x")
     np.testing.assert_array_equal(npi[0], dev[0].cpu().numpy())
+    # the C-ABI host batch entry: pinned and pageable, several chunkings,
+    # every output (indices, stats, sector_of, perm)
+    pinned = torch.from_numpy(xyz).pin_memory()
+    for src, chunks in ((xyz, 0), (pinned, 1), (pinned, 3), (pinned, 10)):
+        h = sample_host_batch(src, 1024, method="npdu_afps", m=8, k=65, sort="x",
+                              return_sector=True, chunks=chunks)
+        for a, b in zip(dev, h):
+            np.testing.assert_array_equal(a.cpu().numpy(), b)
+    h64 = sample_host_batch(xyz.astype(np.float64), 500, method="afps", m=4, first="random",
+                            seed=3, index_dtype=np.int64)
+    d64 = sample(torch.from_numpy(xyz.astype(np.float64)).cuda(), 500, method="afps", m=4,
+                 first="random", seed=3, index_dtype=torch.int64)
+    np.testing.assert_array_equal(h64[0], d64[0].cpu().numpy())
+    np.testing.assert_array_equal(h64[1], d64[1].cpu().numpy())
 
 
 def test_one_million_point_afps_vs_oracle(oracle):
