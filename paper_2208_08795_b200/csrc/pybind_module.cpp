@@ -265,8 +265,11 @@ PYBIND11_MODULE(_core, m) {
         [](int method, int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n,
            std::int64_t c, std::int64_t mm, std::int64_t k, int seed_policy, std::uint64_t seed,
            std::uintptr_t seeds, int index_dtype, std::uintptr_t out_idx, std::uintptr_t out_sector,
-           std::uintptr_t out_stats, int sort_axis, std::uintptr_t out_perm, int chunks) {
+           std::uintptr_t out_stats, int sort_axis, std::uintptr_t out_perm, int chunks,
+           std::int64_t index_base, std::int64_t sector_base) {
           pcs_gpu_args a{};
+          a.index_base = index_base;
+          a.sector_base = sector_base;
           a.method = method;
           a.coord_dtype = coord_dtype;
           a.xyz = reinterpret_cast<const void*>(xyz);
@@ -293,7 +296,8 @@ PYBIND11_MODULE(_core, m) {
         py::arg("method"), py::arg("coord_dtype"), py::arg("xyz"), py::arg("batch"), py::arg("n"),
         py::arg("c"), py::arg("m"), py::arg("k"), py::arg("seed_policy"), py::arg("seed"),
         py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
-        py::arg("out_stats"), py::arg("sort_axis"), py::arg("out_perm"), py::arg("chunks") = 0);
+        py::arg("out_stats"), py::arg("sort_axis"), py::arg("out_perm"), py::arg("chunks") = 0,
+        py::arg("index_base") = 0, py::arg("sector_base") = 0);
   m.def("sort_device",
         [](int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n, int axis,
            std::uintptr_t out_xyz, std::uintptr_t out_perm, std::uintptr_t stream) {

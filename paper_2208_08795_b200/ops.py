@@ -80,8 +80,16 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
     if first not in ("fixed", "random"):
         raise ValueError("first must be 'random' or 'fixed'")
     if isinstance(xyz, torch.Tensor) and not xyz.is_cuda:
-        return _sample_from_host(xyz, c, method, m, k, first, seed, seeds, sort, index_dtype,
-                                 return_sector, index_base, sector_base)
+        # host tensor: the C-ABI host batch entry (pipelined H2D / sort +
+        # sample / D2H in one native call); results come back on the host
+        if index_dtype not in (torch.int32, torch.int64):
+            raise ValueError("index_dtype must be torch.int32 or torch.int64")
+        res = sample_host_batch(xyz, c, method=method, m=m, k=k, first=first, seed=seed,
+                                seeds=seeds, sort=sort,
+                                index_dtype=np.int64 if index_dtype == torch.int64 else np.int32,
+                                return_sector=return_sector, index_base=index_base,
+                                sector_base=sector_base)
+        return tuple(torch.from_numpy(r) for r in res)
     x = _as_batch(xyz)
     perm = None
     if sort is not None:
@@ -111,63 +119,6 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
     if perm is not None:
         out.append(perm)
     return tuple(out)
-
-
-def _sample_from_host(xyz, c, method, m, k, first, seed, seeds, sort, index_dtype,
-                      return_sector, index_base, sector_base, chunks=None, device=None):
-    """Host batch in, host results out, with the H2D copy of chunk i+1
-    overlapping the sort + sample of chunk i (copy stream + compute stream)
-    and each chunk's results copied back as soon as they are ready. Clouds are
-    independent, so chunking by cloud changes nothing in the results."""
-    x = xyz.unsqueeze(0) if xyz.dim() == 2 else xyz
-    if x.dim() != 3 or x.shape[-1] != 3:
-        raise ValueError("expected an (N, 3) or (B, N, 3) tensor")
-    if x.dtype not in (torch.float32, torch.float64):
-        raise ValueError("xyz must be float32 or float64")
-    x = x.contiguous()
-    if not x.is_pinned():
-        x = x.pin_memory()
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    B, N = x.shape[0], x.shape[1]
-    if chunks is None:
-        chunks = max(1, min(int(__import__("os").environ.get("PCS_E2E_CHUNKS", "8")), B))
-    bounds = [(i * B) // chunks for i in range(chunks + 1)]
-    xd = torch.empty(x.shape, dtype=x.dtype, device=dev)
-    outs_host = None
-    main = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    copy.wait_stream(main)  # nothing of this call starts before prior work
-    # chunks run concurrently on a few compute streams: one chunk alone does
-    # not fill the GPU, and the copy engine is the bottleneck anyway
-    workers = [torch.cuda.Stream(dev) for _ in range(min(4, chunks))]
-    done = []
-    for i in range(chunks):
-        b0, b1 = bounds[i], bounds[i + 1]
-        if b1 == b0:
-            continue
-        with torch.cuda.stream(copy):
-            xd[b0:b1].copy_(x[b0:b1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-        ws = workers[i % len(workers)]
-        ws.wait_event(ev)
-        sd = seeds[b0:b1] if seeds is not None else None
-        with torch.cuda.stream(ws):
-            res = sample(xd[b0:b1], c, method=method, m=m, k=k, first=first, seed=seed,
-                         seeds=sd, sort=sort, index_dtype=index_dtype,
-                         return_sector=return_sector, index_base=index_base,
-                         sector_base=sector_base)
-            if outs_host is None:
-                outs_host = [torch.empty((B,) + tuple(t.shape[1:]), dtype=t.dtype).pin_memory()
-                             for t in res]
-            for h, t in zip(outs_host, res):
-                h[b0:b1].copy_(t, non_blocking=True)
-        done.append(res)  # device results stay alive until the copies finish
-    for ws in workers:
-        main.wait_stream(ws)
-    compute = main
-    compute.synchronize()
-    return tuple(outs_host)
 
 
 def quality(xyz: torch.Tensor, idx: torch.Tensor):
@@ -274,8 +225,9 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
 
 def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
                       k: Optional[int] = None, first: str = "fixed", seed: int = 0,
-                      sort: Optional[str] = None, device: str = "cuda",
-                      index_dtype=np.int32, return_sector: bool = False, chunks: int = 0):
+                      sort: Optional[str] = None, device: Optional[str] = None,
+                      index_dtype=np.int32, return_sector: bool = False, chunks: int = 0,
+                      seeds=None, index_base: int = 0, sector_base: int = 0):
     """Host batch in, host results out, through the C-ABI host entry
     ``pcs_sample_host_batch`` (include/pcs_gpu.h): the per-cloud samplers
     over a batch in one native, pipelined call (H2D of a chunk overlaps the
@@ -302,14 +254,24 @@ def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
     stats = torch.empty((B, 4), dtype=torch.int64, pin_memory=pin)
     sec = torch.empty((B, max(int(c), 0)), dtype=torch.int32, pin_memory=pin) if return_sector else None
     perm = torch.empty((B, N), dtype=torch.int32, pin_memory=pin) if sort else None
-    with torch.cuda.device(torch.device(device)):
+    if sort is not None and sort not in _AXES:
+        raise ValueError("axis must be x, y, or z")
+    sd = None
+    if seeds is not None:
+        sd = torch.as_tensor(seeds).to(device="cpu", dtype=torch.int64).contiguous()
+        if sd.numel() != B:
+            raise ValueError("seeds must hold one seed per cloud")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
         _core.sample_host_ptr(METHODS[method], 1 if x.dtype == torch.float64 else 0,
                               x.data_ptr(), B, N, int(c), int(m), int(k) if k is not None else 0,
-                              1 if first == "fixed" else 0, int(seed) & (2**64 - 1), 0,
+                              1 if first == "fixed" else 0, int(seed) & (2**64 - 1),
+                              sd.data_ptr() if sd is not None else 0,
                               1 if idx64 else 0, idx.data_ptr(),
                               sec.data_ptr() if sec is not None else 0, stats.data_ptr(),
                               _AXES[sort] if sort is not None else -1,
-                              perm.data_ptr() if perm is not None else 0, int(chunks))
+                              perm.data_ptr() if perm is not None else 0, int(chunks),
+                              int(index_base), int(sector_base))
     out = [idx.numpy(), stats.numpy()]
     if return_sector:
         out.append(sec.numpy())
