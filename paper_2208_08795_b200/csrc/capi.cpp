@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 #include "pcs_gpu.h"
@@ -147,62 +148,42 @@ int pcs_gpu_sort_axis(int32_t coord_dtype, const void* xyz, int64_t batch, int64
   return e == cudaSuccess ? PCS_OK : cuda_fail(e);
 }
 
-int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int64_t m,
-                    int64_t k, int32_t seed_policy, uint64_t seed, uint32_t threads,
-                    int64_t* out_indices, int64_t* out_sector, uint64_t* out_stats) {
-  (void)threads;  // accepted for pcs::afps(..., threads) parity; GPU schedule is fixed
-  clear_error();
-  std::string msg;
-  int rc = validate_sample(method, n, c, m, k, &msg);
-  if (rc) { set_error(msg); return rc; }
-  cudaStream_t st = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  if (e != cudaSuccess) return cuda_fail(e);
-  {
-    DevBuf dx(st), didx(st), dsec(st), dstat(st);
-    if ((e = dx.alloc(sizeof(double) * 3 * n)) != cudaSuccess ||
-        (e = didx.alloc(sizeof(int64_t) * c)) != cudaSuccess ||
-        (e = dsec.alloc(sizeof(int32_t) * c)) != cudaSuccess ||
-        (e = dstat.alloc(sizeof(uint64_t) * 4)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dx.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
-      rc = cuda_fail(e);
-    } else {
-      pcs_gpu_args a{};
-      a.method = method;
-      a.coord_dtype = PCS_DTYPE_F64;
-      a.xyz = dx.p;
-      a.batch = 1;
-      a.n = n;
-      a.c = c;
-      a.m = m;
-      a.k = k;
-      a.seed_policy = seed_policy;
-      a.seed = seed;
-      a.index_dtype = PCS_INDEX_I64;
-      a.out_indices = didx.p;
-      a.out_sector = static_cast<int32_t*>(dsec.p);
-      a.out_stats = static_cast<uint64_t*>(dstat.p);
-      e = launch_sample(a, st, &msg);
-      if (e != cudaSuccess) {
-        rc = cuda_fail(e, msg);
-      } else {
-        int32_t* sec32 = new int32_t[c];
-        if ((e = cudaMemcpyAsync(out_indices, didx.p, sizeof(int64_t) * c, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(sec32, dsec.p, sizeof(int32_t) * c, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(out_stats, dstat.p, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-            (e = cudaStreamSynchronize(st)) != cudaSuccess) {
-          rc = cuda_fail(e);
-        } else if (out_sector) {
-          for (int64_t i = 0; i < c; ++i) out_sector[i] = sec32[i];
-        }
-        delete[] sec32;
-      }
-    }
+namespace {
+
+// One copy stream + kWorkers compute streams + events per device, created
+// once and kept (creating streams per call costs more than sampling a small
+// batch); host-buffer calls on one device serialise on its mutex.
+constexpr int kWorkers = 4, kEvents = 64;
+struct DevStreams {
+  std::mutex mu;
+  cudaStream_t copy = nullptr, work[kWorkers] = {};
+  cudaEvent_t ev[kEvents] = {};
+  bool ok = false;
+};
+
+cudaError_t device_streams(DevStreams** out) {
+  static std::mutex init_mu;
+  static DevStreams per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  DevStreams& ds = per_dev[dev];
+  std::lock_guard<std::mutex> lock(init_mu);
+  if (!ds.ok) {
+    e = cudaStreamCreateWithFlags(&ds.copy, cudaStreamNonBlocking);
+    for (int w = 0; w < kWorkers && e == cudaSuccess; ++w)
+      e = cudaStreamCreateWithFlags(&ds.work[w], cudaStreamNonBlocking);
+    for (int i = 0; i < kEvents && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&ds.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    ds.ok = true;
   }
-  cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  return rc;
+  *out = &ds;
+  return cudaSuccess;
 }
+
+}  // namespace
 
 int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
                           int32_t chunks) {
@@ -221,32 +202,11 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
   int nch = chunks > 0 ? chunks : 8;
   if (nch > B) nch = static_cast<int>(B);
-  // one copy stream + kWorkers compute streams per device, created once and
-  // kept (stream creation costs more than a small batch's sampling); calls
-  // on the same device are serialised
-  constexpr int kWorkers = 4, kEvents = 64;
-  struct DevStreams {
-    cudaStream_t copy = nullptr, work[kWorkers] = {};
-    cudaEvent_t ev[kEvents] = {};
-    bool ok = false;
-  };
-  static std::mutex mu;
-  static DevStreams per_dev[64];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
-  if (dev >= 64) { set_error("pcs_sample_host_batch: device ordinal >= 64"); return PCS_ERR_UNSUPPORTED; }
-  std::lock_guard<std::mutex> lock(mu);
-  DevStreams& ds = per_dev[dev];
-  if (!ds.ok) {
-    e = cudaStreamCreateWithFlags(&ds.copy, cudaStreamNonBlocking);
-    for (int w = 0; w < kWorkers && e == cudaSuccess; ++w)
-      e = cudaStreamCreateWithFlags(&ds.work[w], cudaStreamNonBlocking);
-    for (int i = 0; i < kEvents && e == cudaSuccess; ++i)
-      e = cudaEventCreateWithFlags(&ds.ev[i], cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(e);
-    ds.ok = true;
-  }
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  DevStreams& ds = *dsp;
   cudaStream_t copy = ds.copy;
   cudaStream_t* work = ds.work;
   if (nch > kEvents - 1) nch = kEvents - 1;
@@ -318,6 +278,63 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
     if (e == cudaSuccess) e = e2;
   }
   if (e != cudaSuccess) return cuda_fail(e, msg);
+  return PCS_OK;
+}
+
+int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int64_t m,
+                    int64_t k, int32_t seed_policy, uint64_t seed, uint32_t threads,
+                    int64_t* out_indices, int64_t* out_sector, uint64_t* out_stats) {
+  (void)threads;  // accepted for pcs::afps(..., threads) parity; GPU schedule is fixed
+  clear_error();
+  std::string msg;
+  int rc = validate_sample(method, n, c, m, k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
+  if (e != cudaSuccess) return cuda_fail(e);
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  cudaStream_t st = dsp->copy;
+  // one workspace: cloud, indices, sector ids (int32 on the device), stats
+  const size_t b_xyz = (sizeof(double) * 3 * n + 255) & ~size_t(255);
+  const size_t b_idx = (sizeof(int64_t) * c + 255) & ~size_t(255);
+  const size_t b_sec = (sizeof(int32_t) * c + 255) & ~size_t(255);
+  void* ws = nullptr;
+  e = workspace_alloc(&ws, b_xyz + b_idx + b_sec + 32, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  char* base = static_cast<char*>(ws);
+  int32_t* dsec = reinterpret_cast<int32_t*>(base + b_xyz + b_idx);
+  uint64_t* dstat = reinterpret_cast<uint64_t*>(base + b_xyz + b_idx + b_sec);
+  std::vector<int32_t> sec32(out_sector ? static_cast<size_t>(c) : 0);
+  e = cudaMemcpyAsync(base, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    pcs_gpu_args a{};
+    a.method = method;
+    a.coord_dtype = PCS_DTYPE_F64;
+    a.xyz = base;
+    a.batch = 1;
+    a.n = n;
+    a.c = c;
+    a.m = m;
+    a.k = k;
+    a.seed_policy = seed_policy;
+    a.seed = seed;
+    a.index_dtype = PCS_INDEX_I64;
+    a.out_indices = base + b_xyz;
+    a.out_sector = out_sector ? dsec : nullptr;
+    a.out_stats = dstat;
+    e = launch_sample(a, st, &msg);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out_indices, base + b_xyz, sizeof(int64_t) * c, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && out_sector)
+    e = cudaMemcpyAsync(sec32.data(), dsec, sizeof(int32_t) * c, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && out_stats)
+    e = cudaMemcpyAsync(out_stats, dstat, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(ws, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, msg);
+  for (int64_t i = 0; out_sector && i < c; ++i) out_sector[i] = sec32[i];
   return PCS_OK;
 }
 
