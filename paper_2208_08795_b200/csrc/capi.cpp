@@ -348,9 +348,11 @@ int pcs_local_fps_host(const double* xyz, int64_t n, int64_t sb, int64_t se, int
   if (k == 0) { set_error("local_fps: window size must be >= 1"); return PCS_ERR_INVALID_ARGUMENT; }
   if (n > 0x7fffffffLL) { set_error("clouds above 2^31-1 points are not supported"); return PCS_ERR_UNSUPPORTED; }
   // k < 0 encodes std::nullopt (full window).
-  cudaStream_t st = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  cudaStream_t st = dsp->copy;
   int rc = PCS_OK;
   const int64_t len = se - sb;
   {
@@ -373,7 +375,6 @@ int pcs_local_fps_host(const double* xyz, int64_t n, int64_t sb, int64_t se, int
       rc = cuda_fail(e, msg);
   }
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   return rc;
 }
 
@@ -382,9 +383,11 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
   clear_error();
   if (axis < 0 || axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
   if (n <= 0) return PCS_OK;
-  cudaStream_t st = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  cudaStream_t st = dsp->copy;
   int rc = PCS_OK;
   {
     DevBuf dx(st), dout(st), dperm(st);
@@ -404,7 +407,6 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
     delete[] perm32;
   }
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   return rc;
 }
 
@@ -440,9 +442,11 @@ static int metric_host(int which, const double* xyz, int64_t n, const int64_t* s
       set_error(std::string(who) + ": index out of range");
       return PCS_ERR_INVALID_ARGUMENT;
     }
-  cudaStream_t st = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  cudaStream_t st = dsp->copy;
   int rc = PCS_OK;
   {
     DevBuf dx(st), di(st), dout(st);
@@ -458,7 +462,6 @@ static int metric_host(int which, const double* xyz, int64_t n, const int64_t* s
       rc = cuda_fail(e);
   }
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   return rc;
 }
 
