@@ -808,6 +808,19 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   if (coord_dtype == PCS_DTYPE_F32 && n > 1024 && n <= 16384) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
+    // few clouds: spread each over a cluster of 2-4 CTAs (the idle SMs
+    // shorten each cloud's network); otherwise one CTA per cloud
+    const char* cs_env = std::getenv("PCS_SORT_SPREAD");
+    const bool spread = !(cs_env && cs_env[0] == '0');
+    if (spread && n > 4096 && batch * 4 <= 148) {
+      if (n <= 8192) return pcsk::launch_reg_sort<2, 4>(x, batch, n, axis, o, out_perm, stream);
+      return pcsk::launch_reg_sort<4, 4>(x, batch, n, axis, o, out_perm, stream);
+    }
+    if (spread && n > 2048 && batch * 2 <= 148) {
+      if (n <= 4096) return pcsk::launch_reg_sort<2, 2>(x, batch, n, axis, o, out_perm, stream);
+      if (n <= 8192) return pcsk::launch_reg_sort<4, 2>(x, batch, n, axis, o, out_perm, stream);
+      return pcsk::launch_reg_sort<8, 2>(x, batch, n, axis, o, out_perm, stream);
+    }
     if (n <= 2048) return pcsk::launch_reg_sort<2>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 4096) return pcsk::launch_reg_sort<4>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 8192) return pcsk::launch_reg_sort<8>(x, batch, n, axis, o, out_perm, stream);

@@ -190,7 +190,7 @@ def test_sort_parity(pcs):
     for name, g in load_sort_goldens().items():
         np.testing.assert_array_equal(pcs.exact_sort(g["points"], "xyz"[int(name[-1])]), g["sorted"])
     rng = np.random.default_rng(3)
-    for n in (1, 2, 17, 1000, 16384, 16385, 40000, 70000, 200000, 300000):
+    for n in (1, 2, 17, 1000, 3000, 5000, 12000, 16384, 16385, 40000, 70000, 200000, 300000):
         xyz = np.round(rng.normal(size=(3, n, 3)), 2).astype(np.float32)
         xyz[:, :: 7, 1] = -0.0
         xyz[:, 1:: 7, 1] = 0.0
