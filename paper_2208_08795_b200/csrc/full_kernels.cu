@@ -166,7 +166,13 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   if (n <= 32) return run_full<1, 1, true>(p, st);
   if (n <= 64) return run_full<2, 1, true>(p, st);
   if (n <= 128) return run_full<4, 1, true>(p, st);
-  if (n <= 256) return run_full<8, 1, true>(p, st);
+  if (n <= 256) {
+    // one sector per SM or fewer: 4 warps x 2 slots shorten the serial chain
+    // (cfg2 0.032 -> 0.027 ms); with many sectors one warp each wins
+    // (AFPS M=16 at 4K: 0.098 vs 0.157 ms)
+    if (p.B * p.M <= 148) return run_full<2, 4, true>(p, st);
+    return run_full<8, 1, true>(p, st);
+  }
   // 8 slots per thread (twice the warps, ~120 registers) hides more latency
   // when an SM holds one sector or at least four; with ~2 sectors per SM the
   // 16-slot form measured faster (r01 sweep: cfg5 FPS 2K 0.374 vs 0.400 ms;
