@@ -38,6 +38,14 @@ using namespace rows;
 
 namespace {
 
+// Z-order cells of ~8 points for the slot bucketing: 2^bits cells, 32 to
+// 4096 (a multiple of 32 for the one-warp scan)
+__host__ __device__ __forceinline__ int morton_cell_bits(int np) {
+  int b = 5;
+  while (b < 12 && (1 << b) * 8 < np) ++b;
+  return b;
+}
+
 __device__ __forceinline__ void tm_row_ld(uint32_t a, double& d, uint32_t& orig) {
   uint32_t r[4];
   tm_ld(a, r);
@@ -79,6 +87,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   Msg* xbuf = reinterpret_cast<Msg*>(cand + 2 * W);                               // [2][CS * W]
   uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + (CS > 1 ? 2 * CS * W : 0));  // [2]
   int* scratch = reinterpret_cast<int*>(xbar + 2);                                 // [8]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(scratch + 8);  // [1 << morton_cell_bits]
   if (p.f64) __trap();
   auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
 
@@ -121,21 +130,28 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
     }
   }
   __syncthreads();
-  // ---- 2. Morton keys (code << 32 | storage slot) over the xs/ys region
-  unsigned long long* key = reinterpret_cast<unsigned long long*>(xs);
+  // ---- 2./3. slot order: storage order (WIN) or a Z-order bucketing --
+  //         counting sort of the points by the top bits of their Morton
+  //         code (cells of ~8 points; order inside a cell is whatever the
+  //         shared-memory atomics give -- any order is exact, only the row
+  //         boxes' compactness depends on it)
+  uint32_t* src_slot = reinterpret_cast<uint32_t*>(zs);
   if constexpr (WIN) {
-    for (int jl = threadIdx.x; jl < np; jl += T) {
-      const int gj = to_sector(jl);
-      key[jl] = ((jl >> 5) < srows_local && gj < n) ? static_cast<unsigned long long>(jl) : ~0ull;
-    }
+    for (int i = threadIdx.x; i < np; i += T) src_slot[i] = static_cast<uint32_t>(i);
   } else {
+    const int cb = morton_cell_bits(np);
+    const int cells = 1 << cb;
+    uint32_t* rank_of = reinterpret_cast<uint32_t*>(xs);
+    uint32_t* cell_of = reinterpret_cast<uint32_t*>(ys);
+    for (int i = threadIdx.x; i < cells; i += T) hist[i] = 0u;
+    __syncthreads();
     const float bx0 = ord2f(scratch[0]), by0 = ord2f(scratch[2]), bz0 = ord2f(scratch[4]);
     const float ext = fmaxf(fmaxf(ord2f(scratch[1]) - bx0, ord2f(scratch[3]) - by0),
                             ord2f(scratch[5]) - bz0);
     const float sc = (ext > 0.f && ext < INFINITY) ? 1023.0f / ext : 0.f;
     for (int jl = threadIdx.x; jl < np; jl += T) {
       const int gj = to_sector(jl);
-      unsigned long long k = ~0ull;
+      uint32_t cell = kNoIndex;
       if ((jl >> 5) < srows_local && gj < n) {
         const float* q = cloud + 3LL * gj;
         auto qz = [&](float c, float c0) {
@@ -143,32 +159,39 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
           return spread3(static_cast<uint32_t>(t));
         };
         const uint32_t code = qz(q[0], bx0) | (qz(q[1], by0) << 1) | (qz(q[2], bz0) << 2);
-        k = (static_cast<unsigned long long>(code) << 32) | static_cast<uint32_t>(jl);
+        cell = code >> (30 - cb);
+        rank_of[jl] = atomicAdd(&hist[cell], 1u);
       }
-      key[jl] = k;
+      cell_of[jl] = cell;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the cell counts (cells / 32 per lane)
+      const int per = cells >> 5;
+      uint32_t sum = 0;
+      for (int i = 0; i < per; ++i) sum += hist[lane * per + i];
+      uint32_t x = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x += y;
+      }
+      uint32_t run = x - sum;
+      for (int i = 0; i < per; ++i) {
+        const uint32_t c = hist[lane * per + i];
+        hist[lane * per + i] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    for (int jl = threadIdx.x; jl < np; jl += T) {
+      const uint32_t cell = cell_of[jl];
+      if (cell != kNoIndex) src_slot[hist[cell] + rank_of[jl]] = static_cast<uint32_t>(jl);
     }
   }
   __syncthreads();
-  // ---- 3. bitonic sort (non-power-of-two size: mirrored first merge step)
-  for (int kk = 2; kk < (WIN ? 0 : 2 * np); kk <<= 1) {
-    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      const int mask = jj == (kk >> 1) ? kk - 1 : jj;
-      for (int i = threadIdx.x; i < np; i += T) {
-        const int pi = i ^ mask;
-        if (pi > i && pi < np) {
-          const unsigned long long a = key[i], c = key[pi];
-          if (a > c) { key[i] = c; key[pi] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // ---- 4. slot -> storage slot into the zs region, then each warp gathers
-  //         its rows' coordinates (from L2) and writes d / index to TMEM
+  // ---- 4. each warp gathers its rows' coordinates (from L2) and writes
+  //         d / index to TMEM
   {
-    uint32_t* src_slot = reinterpret_cast<uint32_t*>(zs);
-    for (int i = threadIdx.x; i < np; i += T) src_slot[i] = static_cast<uint32_t>(key[i]);
-    __syncthreads();
     for (int l = 0; l < rpw; ++l) {
       const int i = ((warp + W * l) << 5) + lane;
       const uint32_t jl = src_slot[i];
@@ -472,6 +495,7 @@ size_t morton_tmem_smem(int np, int W, int CS) {
   bytes += 2 * W * sizeof(uint4);
   bytes += CS > 1 ? 2 * CS * W * sizeof(Msg) : 0;
   bytes += 2 * sizeof(uint64_t) + 8 * sizeof(int);
+  bytes += sizeof(uint32_t) << morton_cell_bits(np);  // bucketing histogram
   return bytes;
 }
 
