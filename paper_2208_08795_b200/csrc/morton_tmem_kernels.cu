@@ -40,9 +40,12 @@ namespace {
 
 // Z-order cells of ~8 points for the slot bucketing: 2^bits cells, 32 to
 // 4096 (a multiple of 32 for the one-warp scan)
+#ifndef MORTON_CELL_PTS
+#define MORTON_CELL_PTS 8
+#endif
 __host__ __device__ __forceinline__ int morton_cell_bits(int np) {
   int b = 5;
-  while (b < 12 && (1 << b) * 8 < np) ++b;
+  while (b < 12 && (1 << b) * MORTON_CELL_PTS < np) ++b;
   return b;
 }
 
