@@ -37,6 +37,13 @@ namespace pcsk {
 using namespace rows;
 
 
+// Z-order cells of ~8 points for the slot bucketing (2^5 .. 2^12 cells)
+__host__ __device__ __forceinline__ int morton_smem_cell_bits(int np) {
+  int b = 5;
+  while (b < 12 && (1 << b) * 8 < np) ++b;
+  return b;
+}
+
 // Local slot layout: the CTA's storage points (sector rows R % CS == rank,
 // interleaved as in rows_kernel) sorted by Morton code; slots [0, held) hold
 // points, rows of 32 slots. Local row r belongs to warp r % W, lane r / W.
@@ -63,6 +70,7 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
   Msg* xbuf = reinterpret_cast<Msg*>(cand + 2 * W);              // [2][CS * W]
   uint64_t* xbar = reinterpret_cast<uint64_t*>(xbuf + (CS > 1 ? 2 * CS * W : 0));  // [2]
   int* scratch = reinterpret_cast<int*>(xbar + 2);                // [8]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(scratch + 8);      // bucketing histogram
   if (sizeof(CT) < sizeof(double) && p.f64) __trap();
   auto to_sector = [&](int jl) { return (((jl >> 5) * CS + rank) << 5) + (jl & 31); };
 
@@ -109,46 +117,61 @@ __global__ void __launch_bounds__(W * 32) morton_rows_kernel(const SampleParams 
     const int last_R = (srows_local - 1) * CS + rank;
     held = (srows_local - 1) * 32 + min(32, n - last_R * 32);
   }
-  // ---- 2. Morton keys (code << 32 | storage slot), empty slots last
-  unsigned long long* key = reinterpret_cast<unsigned long long*>(d);
+  // ---- 2./3. Z-order bucketing: counting sort of the points by the top
+  //         bits of their Morton code (cells of ~8 points; the order inside
+  //         a cell is the shared-memory atomics' -- any order is exact).
+  //         orig[slot] = storage slot, kNoIndex past the points
   {
+    const int cb = morton_smem_cell_bits(np);
+    const int cells = 1 << cb;
+    uint32_t* rank_of = reinterpret_cast<uint32_t*>(d);
+    uint32_t* cell_of = rank_of + np;
+    for (int i = threadIdx.x; i < cells; i += T) hist[i] = 0u;
+    for (int i = threadIdx.x; i < np; i += T) orig[i] = kNoIndex;
+    __syncthreads();
     const float bx0 = ord2f(scratch[0]), by0 = ord2f(scratch[2]), bz0 = ord2f(scratch[4]);
     const float ext = fmaxf(fmaxf(ord2f(scratch[1]) - bx0, ord2f(scratch[3]) - by0),
                             ord2f(scratch[5]) - bz0);
     const float sc = (ext > 0.f && ext < INFINITY) ? 1023.0f / ext : 0.f;
     for (int jl = threadIdx.x; jl < np; jl += T) {
       const int gj = to_sector(jl);
-      const bool valid = (jl >> 5) < srows_local && gj < n;
-      unsigned long long k = ~0ull;
-      if (valid) {
+      uint32_t cell = kNoIndex;
+      if ((jl >> 5) < srows_local && gj < n) {
         auto q = [&](CT c, float c0) {
           const float t = fminf(fmaxf((static_cast<float>(c) - c0) * sc, 0.f), 1023.f);
           return spread3(static_cast<uint32_t>(t));
         };
         const uint32_t code = q(xs[jl], bx0) | (q(ys[jl], by0) << 1) | (q(zs[jl], bz0) << 2);
-        k = (static_cast<unsigned long long>(code) << 32) | static_cast<uint32_t>(jl);
+        cell = code >> (30 - cb);
+        rank_of[jl] = atomicAdd(&hist[cell], 1u);
       }
-      key[jl] = k;
+      cell_of[jl] = cell;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the cell counts (cells / 32 per lane)
+      const int per = cells >> 5;
+      uint32_t sum = 0;
+      for (int i = 0; i < per; ++i) sum += hist[lane * per + i];
+      uint32_t x = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x += y;
+      }
+      uint32_t run = x - sum;
+      for (int i = 0; i < per; ++i) {
+        const uint32_t c = hist[lane * per + i];
+        hist[lane * per + i] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    for (int jl = threadIdx.x; jl < np; jl += T) {
+      const uint32_t cell = cell_of[jl];
+      if (cell != kNoIndex) orig[hist[cell] + rank_of[jl]] = static_cast<uint32_t>(jl);
     }
   }
-  __syncthreads();
-  // ---- 3. bitonic sort of np keys (np need not be a power of two: the
-  //         mirrored first step of every merge treats missing slots as +inf)
-  for (int kk = 2; kk < 2 * np; kk <<= 1) {
-    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      const int mask = jj == (kk >> 1) ? kk - 1 : jj;
-      for (int i = threadIdx.x; i < np; i += T) {
-        const int pi = i ^ mask;
-        if (pi > i && pi < np) {
-          const unsigned long long a = key[i], c = key[pi];
-          if (a > c) { key[i] = c; key[pi] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // ---- 4. permute coordinates (d[] is the scratch row), build orig[]
-  for (int i = threadIdx.x; i < np; i += T) orig[i] = static_cast<uint32_t>(key[i]);
+  // ---- 4. permute coordinates (d[] is the scratch row)
   __syncthreads();
   {
     CT* tmp = reinterpret_cast<CT*>(d);
@@ -466,6 +489,7 @@ size_t morton_smem_bytes(int np, int W, int CS) {
   bytes += 2 * W * sizeof(uint4);
   bytes += CS > 1 ? 2 * CS * W * sizeof(Msg) : 0;
   bytes += 2 * sizeof(uint64_t) + 8 * sizeof(int);
+  bytes += sizeof(uint32_t) << morton_smem_cell_bits(np);
   return bytes;
 }
 

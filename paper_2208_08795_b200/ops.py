@@ -156,9 +156,18 @@ def _morton_fits(n: int, dtype: str) -> bool:
         nbytes = np_ * (8 + 3 * ct + 4) + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
         nbytes += 2 * cs * w * 48 if cs > 1 else 0
         nbytes += 2 * 8 + 8 * 4
+        nbytes += 4 * _cells(np_)
         if nbytes <= 227 * 1024:
             return True
     return False
+
+
+def _cells(np_: int) -> int:
+    """Bucketing histogram size (morton_*cell_bits): 2^5 .. 2^12 cells of ~8."""
+    b = 5
+    while b < 12 and (1 << b) * 8 < np_:
+        b += 1
+    return 1 << b
 
 
 def _morton_tmem_fits(n: int) -> bool:
@@ -173,6 +182,7 @@ def _morton_tmem_fits(n: int) -> bool:
         nbytes = np_ * 12 + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
         nbytes += 2 * cs * w * 48 if cs > 1 else 0
         nbytes += 2 * 8 + 8 * 4
+        nbytes += 4 * _cells(np_)
         if nbytes <= 227 * 1024:
             return True
     return False

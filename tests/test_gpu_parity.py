@@ -6,6 +6,8 @@ operation order, no FMA -> identical bits). Everything goes through the
 C-ABI: the drop-in Python surface (pcs.fps, ...) calls pcs_sample_host, the
 batched torch op calls pcs_gpu_sample / pcs_gpu_sort_axis.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -470,7 +472,8 @@ def test_busy_afps_takes_morton_engine(oracle):
     from paper_2208_08795_b200 import sample
 
     B, n, m, c = 150, 4400, 4, 1000
-    assert pcs.kernel_family("afps", n, m, batch=B) == "morton_tmem_kernel"
+    if os.environ.get("PCS_MORTON_TMEM", "1") != "0":
+        assert pcs.kernel_family("afps", n, m, batch=B) == "morton_tmem_kernel"
     xyz = synth.stable_sort_np(synth.primitives(B, n, 5, seed=12), 0)[0]
     idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="afps", m=m, first="random", seed=2)
     want_idx, want_st = oracle.sample_batch_f32("afps", xyz, c, m, 0, "random", 2)
