@@ -71,11 +71,37 @@ __device__ __forceinline__ void write_index(const SampleParams& p, long long b, 
 template <typename Tin, typename CT>
 __device__ __forceinline__ void stage_sector(const Tin* __restrict__ src, int n, CT* xs, CT* ys,
                                              CT* zs, int t, int nthreads) {
-  for (int e = t; e < 3 * n; e += nthreads) {
-    const CT v = static_cast<CT>(src[e]);
+  auto put = [&](int e, Tin v) {
     const int q = e / 3, a = e - 3 * q;
-    (a == 0 ? xs : (a == 1 ? ys : zs))[q] = v;
+    (a == 0 ? xs : (a == 1 ? ys : zs))[q] = static_cast<CT>(v);
+  };
+  int e0 = 0;
+  if constexpr (sizeof(Tin) == 4) {
+    // 16-byte loads, four in flight per thread: a sector is a few KB of
+    // contiguous AoS, staging is load-latency bound otherwise
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      const int n4 = (3 * n) >> 2;
+      int i = t;
+      for (; i + 3 * nthreads < n4; i += 4 * nthreads) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(s4 + i + u * nthreads);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = 4 * (i + u * nthreads);
+          put(e, v[u].x); put(e + 1, v[u].y); put(e + 2, v[u].z); put(e + 3, v[u].w);
+        }
+      }
+      for (; i < n4; i += nthreads) {
+        const float4 v = __ldg(s4 + i);
+        const int e = 4 * i;
+        put(e, v.x); put(e + 1, v.y); put(e + 2, v.z); put(e + 3, v.w);
+      }
+      e0 = 4 * n4;
+    }
   }
+  for (int e = e0 + t; e < 3 * n; e += nthreads) put(e, src[e]);
 }
 
 template <int W>
