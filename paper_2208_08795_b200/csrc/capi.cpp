@@ -294,8 +294,30 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
   if (e != cudaSuccess) return cuda_fail(e);
   std::lock_guard<std::mutex> lock(dsp->mu);
   cudaStream_t st = dsp->copy;
+  // Full-window samplers on coordinates that are all exactly representable
+  // in fp32 (the usual case: clouds read from f32_bin files or float32
+  // arrays, forcecast to float64 by the binding) run from an fp32 copy: the
+  // kernels widen fp32 exactly, so every distance and every result is the
+  // same, the copy is halved and large sectors get the tensor-memory Morton
+  // engine. (Windowed samplers keep fp64 staging: one cloud's NPDU sectors
+  // are latency-bound and fp64 coordinates need no per-iteration widening.)
+  std::vector<float> f32;
+  const bool windowed = method == PCS_METHOD_NPDU_FPS || method == PCS_METHOD_NPDU_AFPS;
+  if (!windowed) {
+    bool exact = true;
+    for (int64_t i = 0; i < 3 * n && exact; ++i) {
+      const float f = static_cast<float>(xyz[i]);
+      exact = static_cast<double>(f) == xyz[i];  // NaN: not exact
+    }
+    if (exact) {
+      f32.resize(static_cast<size_t>(3 * n));
+      for (int64_t i = 0; i < 3 * n; ++i) f32[i] = static_cast<float>(xyz[i]);
+    }
+  }
+  const bool use32 = !f32.empty() || n == 0;
+  const size_t coord_bytes = (use32 ? sizeof(float) : sizeof(double)) * 3 * n;
   // one workspace: cloud, indices, sector ids (int32 on the device), stats
-  const size_t b_xyz = (sizeof(double) * 3 * n + 255) & ~size_t(255);
+  const size_t b_xyz = (coord_bytes + 255) & ~size_t(255);
   const size_t b_idx = (sizeof(int64_t) * c + 255) & ~size_t(255);
   const size_t b_sec = (sizeof(int32_t) * c + 255) & ~size_t(255);
   void* ws = nullptr;
@@ -305,11 +327,12 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
   int32_t* dsec = reinterpret_cast<int32_t*>(base + b_xyz + b_idx);
   uint64_t* dstat = reinterpret_cast<uint64_t*>(base + b_xyz + b_idx + b_sec);
   std::vector<int32_t> sec32(out_sector ? static_cast<size_t>(c) : 0);
-  e = cudaMemcpyAsync(base, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st);
+  e = cudaMemcpyAsync(base, use32 ? static_cast<const void*>(f32.data()) : static_cast<const void*>(xyz),
+                      coord_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     pcs_gpu_args a{};
     a.method = method;
-    a.coord_dtype = PCS_DTYPE_F64;
+    a.coord_dtype = use32 ? PCS_DTYPE_F32 : PCS_DTYPE_F64;
     a.xyz = base;
     a.batch = 1;
     a.n = n;

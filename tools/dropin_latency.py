@@ -20,3 +20,13 @@ for n, c, m, k in ((2048, 512, 8, None), (2048, 512, 1, None), (32768, 8192, 32,
         f()
         ts.append((time.perf_counter() - t0) * 1e3)
     print(n, c, m, k, "ms/call median %.3f min %.3f" % (float(np.median(ts)), min(ts)))
+for n, c in ((8192, 2048), (32768, 1024)):
+    pts = synth.uniform_cube(1, n, 2)[0].astype(np.float64)
+    for _ in range(3):
+        pcs.fps(pts, c)
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        pcs.fps(pts, c)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print("fps", n, c, "ms/call median %.3f" % float(np.median(ts)))
