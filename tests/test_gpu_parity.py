@@ -333,7 +333,7 @@ def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
 
 
 @pytest.mark.parametrize("tmem", ["1", "0"])
-@pytest.mark.parametrize("cloud", ["cube", "primitives", "dupes", "f64"])
+@pytest.mark.parametrize("cloud", ["cube", "primitives", "dupes", "f64", "f64exact"])
 def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
     """Full-window sectors past 3072 points take the Morton-row engines (CTA
     Morton sort, orig-index row keys; per-point state in TMEM for fp32 input,
@@ -344,7 +344,7 @@ def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
     from paper_2208_08795_b200 import sample
 
     monkeypatch.setenv("PCS_MORTON_TMEM", tmem)
-    if cloud == "f64" and tmem == "0":
+    if cloud in ("f64", "f64exact") and tmem == "0":
         pytest.skip("fp64 input always uses the shared-memory engine")
 
     for n, c, m in ((8192, 2048, 1), (16384, 1500, 1), (32768, 700, 1), (60000, 300, 1),
@@ -356,8 +356,11 @@ def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
         if cloud == "dupes":
             xyz[0, 1::3] = xyz[0, 0]
             xyz[0, 2::7] = xyz[0, 5]
-        if cloud == "f64":
-            pts = synth.random_cloud(n, n)
+        if cloud in ("f64", "f64exact"):
+            # f64exact: float64 holding fp32 values -> the drop-in samples
+            # from an fp32 copy (same results by construction)
+            pts = (synth.random_cloud(n, n) if cloud == "f64" else
+                   xyz[0].astype(np.float64))
             got = pcs.afps(pts, c, m, seed=n) if m > 1 else pcs.fps(pts, c, seed=n)
             want = oracle.sample("afps" if m > 1 else "fps", pts, c, m, first="random", seed=n)
             _same(got, *want)
