@@ -319,9 +319,19 @@ __global__ void __launch_bounds__(kSortThreads)
       float v[3 * E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        v[3 * e] = src[3LL * from[e]];
-        v[3 * e + 1] = src[3LL * from[e] + 1];
-        v[3 * e + 2] = src[3LL * from[e] + 2];
+        // the point's 12 bytes from two aligned 8-byte loads (16 bytes
+        // starting at the even float index at or below 3 * from)
+        const long long i0 = 3LL * from[e];
+        if (from[e] == N - 1) {  // the 16 bytes could run past the cloud
+          v[3 * e] = src[i0]; v[3 * e + 1] = src[i0 + 1]; v[3 * e + 2] = src[i0 + 2];
+          continue;
+        }
+        const float2* q = reinterpret_cast<const float2*>(src + (i0 & ~1LL));
+        const float2 a = __ldg(q), c = __ldg(q + 1);
+        const bool odd = i0 & 1;
+        v[3 * e] = odd ? a.y : a.x;
+        v[3 * e + 1] = odd ? c.x : a.y;
+        v[3 * e + 2] = odd ? c.y : c.x;
       }
       float4* dp = reinterpret_cast<float4*>(dst + 3 * g0);
 #pragma unroll
