@@ -7,7 +7,9 @@
 // equal, so stability must keep their storage order). NaN is excluded by
 // the reference's precondition (proj/src/point_cloud.cpp:43-50).
 //
-// * fp32, N <= 16384: one CTA per cloud sorts packed (key << 32 | index)
+// * fp32, N <= 4096, and up to 37 clouds of <= 65536: the on-chip LSD radix
+//   (radix_reg_kernel, end of this file; a cluster of CTAs for N > 4096).
+// * fp32, N <= 16384 otherwise: one CTA per cloud sorts packed (key << 32 | index)
 //   words with a bitonic network in shared memory. Packing the storage index
 //   into the low bits makes every word unique and orders ties by index, so an
 //   unstable network yields exactly the stable order.
@@ -808,6 +810,201 @@ cudaError_t launch_device_radix(const T* xyz, long long batch, long long n, int 
   return e != cudaSuccess ? e : e2;
 }
 
+// ------------------------------------------------------ on-chip radix sort
+// Stable LSD radix (8-bit digits, 4 passes over the 32-bit order key) of a
+// cloud held on chip: a CTA of NT threads keeps E keys + storage indices
+// per thread in registers; CS > 1 spreads the cloud over a thread-block
+// cluster (CS * NT * E points), exchanging digit totals and scattering
+// through DSMEM. Layout: warp w of cluster rank r owns the contiguous
+// segment g = (r * NT/32 + w) * 32E + e * 32 + lane (striped across lanes, so
+// the order inside a warp is e-major, lane-minor). Per pass:
+//   rank   per key: eight ballots on the digit give the lanes sharing it;
+//          the warp's private count hist[w][d] before this key + the peers
+//          at lower lanes = the key's rank inside the warp's digit run
+//          (segment order = storage order, so every pass is stable);
+//   scan   offsets[w][d] = keys with a smaller digit (whole cloud) + keys
+//          with digit d in earlier CTAs + in earlier warps of this CTA;
+//   scatter key/index to offsets[w][d] + rank (local or remote shared
+//          memory), barrier, read back the striped segment.
+// Passes whose digit is the same for every key are the identity: skipped.
+// Padding slots (g >= N) carry the key 0xffffffff (a NaN pattern, excluded
+// by the reference's precondition), so they stay behind every real key.
+// lanes holding the same 8-bit digit: one ballot per bit (MATCH.ANY has a
+// long, poorly pipelined latency -- it bounded the first version of this
+// kernel, ncu short_scoreboard stalls on its consumers)
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+  unsigned peers = kFull;
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const unsigned bb = __ballot_sync(kFull, (d >> bit) & 1u);
+    peers &= ((d >> bit) & 1u) ? bb : ~bb;
+  }
+  return peers;
+}
+
+template <int NT, int E, int CS, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    radix_reg_kernel(const float* __restrict__ xyz, long long N, int axis,
+                     float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  constexpr int NW = NT / 32, NP = NT * E, P = NT / 256;  // P threads per digit in the scan
+  static_assert(NT % 256 == 0 && NW / P == 8, "scan layout: 8 warps per scan thread");
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* sk = smem;                 // NP keys
+  uint32_t* si = smem + NP;            // NP indices
+  uint32_t* hist = smem + 2 * NP;      // [NW][256]
+  uint32_t* ctot = hist + 256 * NW;    // [2][256] this CTA's digit totals (cluster form),
+                                       // double-buffered by pass parity
+  uint32_t* wsum = ctot + 512;         // [NW]
+  __shared__ int identity;
+  const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const long long b = blockIdx.x / CS;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t* hw = hist + w * 256;       // this warp's digit counts, then offsets
+  const float* src = xyz + b * N * 3;
+  const long long seg = (static_cast<long long>(rank) * NW + w) * (32 * E) + lane;
+  constexpr long long T = static_cast<long long>(NP) * CS;
+
+  uint32_t key[E], idx[E], rk[E / 2];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long g = seg + 32 * e;
+    key[e] = g < N ? order_key(__ldg(src + 3 * g + axis)) : 0xffffffffu;
+    idx[e] = static_cast<uint32_t>(g);
+  }
+  for (int shift = 0; shift < 32; shift += 8) {
+    for (int i = t; i < 256 * NW; i += NT) hist[i] = 0;
+    if (t == 0) identity = 0;
+    __syncthreads();
+    // rank inside the warp's digit run
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t d = (key[e] >> shift) & 255u;
+      const unsigned peers = digit_peers(d);
+      const uint32_t before = hw[d];
+      __syncwarp();
+      if ((peers & lt_mask) == 0) hw[d] = before + __popc(peers);
+      __syncwarp();
+      const uint32_t r = before + __popc(peers & lt_mask);
+      if (e & 1) rk[e >> 1] |= r << 16; else rk[e >> 1] = r;
+    }
+    __syncthreads();
+    // scan: thread (d, q) owns warps 8q .. 8q+7 of digit d
+    const int d = t / P, q = t % P;
+    uint32_t* h = hist + 8 * q * 256 + d;
+    uint32_t ex[8], s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { ex[i] = s; s += h[256 * i]; }
+    uint32_t pre = s;  // inclusive over q inside the digit's P threads
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, pre, o, P);
+      if (q >= o) pre += v;
+    }
+    uint32_t tot = __shfl_sync(kFull, pre, P - 1, P);
+    pre -= s;  // exclusive over q
+    uint32_t rpre = 0;  // digit d in earlier CTAs of the cluster
+    if constexpr (CS > 1) {
+      uint32_t* ct = ctot + ((shift >> 3) & 1) * 256 + d;
+      if (q == 0) *ct = tot;
+      cg::this_cluster().sync();
+      uint32_t g = 0;
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        const uint32_t v = *cg::this_cluster().map_shared_rank(ct, r);
+        rpre += r < rank ? v : 0u;
+        g += v;
+      }
+      tot = g;
+    }
+    // digits with a smaller value: inclusive scan of tot over the digits
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = P; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    if (q == 0 && tot == static_cast<uint32_t>(T)) identity = 1;
+    __syncthreads();
+    uint32_t wb = lane < NW ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, wb, o);
+      if (lane >= o) wb += v;
+    }
+    const uint32_t wbase = w > 0 ? __shfl_sync(kFull, wb, (w - 1) & 31) : 0u;
+    const uint32_t dbase = wbase + inc - tot + rpre + pre;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[256 * i] = dbase + ex[i];
+    const int skip = identity;
+    __syncthreads();
+    if (skip) continue;
+    // scatter
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t dd = (key[e] >> shift) & 255u;
+      const uint32_t r = (e & 1) ? rk[e >> 1] >> 16 : rk[e >> 1] & 0xffffu;
+      const uint32_t pos = hw[dd] + r;
+      if constexpr (CS > 1) {
+        const int dst = static_cast<int>(pos / NP);
+        const uint32_t lp = pos % NP;
+        *cg::this_cluster().map_shared_rank(sk + lp, dst) = key[e];
+        *cg::this_cluster().map_shared_rank(si + lp, dst) = idx[e];
+      } else {
+        sk[pos] = key[e];
+        si[pos] = idx[e];
+      }
+    }
+    if constexpr (CS > 1) cg::this_cluster().sync(); else __syncthreads();
+    const int lb = w * 32 * E + lane;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      key[e] = sk[lb + 32 * e];
+      idx[e] = si[lb + 32 * e];
+    }
+  }
+  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long g = seg + 32 * e;
+    if (g < N) {
+      if (out_perm) out_perm[b * N + g] = static_cast<int>(idx[e]);
+      if (dst) gather_point(src, dst, g, idx[e]);
+    }
+  }
+  if constexpr (CS > 1) cg::this_cluster().sync();  // no CTA leaves while partners may read it
+}
+
+template <int NT, int E, int CS = 1, int MINB = 1>
+cudaError_t launch_radix_reg(const float* xyz, long long batch, long long n, int axis,
+                             float* out_xyz, int* out_perm, cudaStream_t st) {
+  constexpr int NW = NT / 32;
+  const size_t smem = sizeof(uint32_t) * (2 * NT * E + 256 * NW + 512 + NW);
+  auto kern = radix_reg_kernel<NT, E, CS, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * CS));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace pcsk
 
 namespace pcs_internal {
@@ -815,6 +1012,31 @@ namespace pcs_internal {
 cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t n, int axis,
                         void* out_xyz, int32_t* out_perm, cudaStream_t stream) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
+  // On-chip radix (radix_reg_kernel) where it beats the bitonic networks
+  // (tools/sort_ab.py on a B200): every cloud of <= 4096 points (256 x 4K:
+  // 0.051 -> 0.035 ms), and few larger clouds, spread over a cluster of
+  // 2K-point (<= 16 clouds) or 4K-point (<= 37 clouds) CTAs: 4 x 32K 0.133 ->
+  // 0.037 ms, 37 x 8K 0.047 -> 0.035 ms. Many large clouds keep the bitonic
+  // network (one or two CTAs per cloud, no cross-CTA scatter): 64 x 16K
+  // 0.064 vs 0.082, 256 x 32K 0.53 vs 0.63.
+  const char* radix_env = std::getenv("PCS_SORT_RADIX");
+  const bool radix_off = radix_env && radix_env[0] == '0';
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && (n <= 4096 || (batch <= 37 && n <= 65536))) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    if (n <= 1024) return pcsk::launch_radix_reg<256, 4, 1, 4>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 2048) return pcsk::launch_radix_reg<256, 8, 1, 4>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 4096) return pcsk::launch_radix_reg<512, 8, 1, 2>(x, batch, n, axis, o, out_perm, stream);
+    if (batch <= 16 && n <= 32768) {
+      if (n <= 8192) return pcsk::launch_radix_reg<256, 8, 4, 4>(x, batch, n, axis, o, out_perm, stream);
+      if (n <= 16384) return pcsk::launch_radix_reg<256, 8, 8, 4>(x, batch, n, axis, o, out_perm, stream);
+      return pcsk::launch_radix_reg<256, 8, 16, 4>(x, batch, n, axis, o, out_perm, stream);
+    }
+    if (n <= 8192) return pcsk::launch_radix_reg<512, 8, 2, 2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 16384) return pcsk::launch_radix_reg<512, 8, 4, 2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 32768) return pcsk::launch_radix_reg<512, 8, 8, 2>(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_radix_reg<512, 8, 16, 2>(x, batch, n, axis, o, out_perm, stream);
+  }
   if (coord_dtype == PCS_DTYPE_F32 && n > 1024 && n <= 16384) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
