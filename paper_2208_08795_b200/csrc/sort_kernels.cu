@@ -8,7 +8,9 @@
 // the reference's precondition (proj/src/point_cloud.cpp:43-50).
 //
 // * fp32, N <= 4096, and up to 37 clouds of <= 65536: the on-chip LSD radix
-//   (radix_reg_kernel, end of this file; a cluster of CTAs for N > 4096).
+//   (radix_reg_kernel, end of this file; a cluster of CTAs for N > 4096);
+//   148+ clouds of <= 32768: radix_cta_kernel (one CTA per cloud, or a
+//   2-CTA cluster merging its sorted halves).
 // * fp32, N <= 16384 otherwise: one CTA per cloud sorts packed (key << 32 | index)
 //   words with a bitonic network in shared memory. Packing the storage index
 //   into the low bits makes every word unique and orders ties by index, so an
@@ -1005,6 +1007,218 @@ cudaError_t launch_radix_reg(const float* xyz, long long batch, long long n, int
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// CTA-local digit offsets: hist[w][d] (per-warp digit counts) becomes the
+// position of warp w's first key with digit d in the CTA's output order.
+// Returns whether one digit holds all NP keys (the pass is the identity).
+template <int NT>
+__device__ __forceinline__ bool cta_digit_offsets(uint32_t* hist, uint32_t* wsum, int* flag,
+                                                  uint32_t np) {
+  constexpr int NW = NT / 32, P = NT / 256;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int d = t / P, q = t % P;
+  uint32_t* h = hist + 8 * q * 256 + d;
+  uint32_t ex[8], s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { ex[i] = s; s += h[256 * i]; }
+  uint32_t pre = s;
+#pragma unroll
+  for (int o = 1; o < P; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, pre, o, P);
+    if (q >= o) pre += v;
+  }
+  const uint32_t tot = __shfl_sync(kFull, pre, P - 1, P);
+  pre -= s;
+  uint32_t inc = tot;
+#pragma unroll
+  for (int o = P; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[w] = inc;
+  if (q == 0 && tot == np) *flag = 1;
+  __syncthreads();
+  uint32_t wb = lane < NW ? wsum[lane] : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, wb, o);
+    if (lane >= o) wb += v;
+  }
+  const uint32_t wbase = w > 0 ? __shfl_sync(kFull, wb, (w - 1) & 31) : 0u;
+  const uint32_t dbase = wbase + inc - tot + pre;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[256 * i] = dbase + ex[i];
+  const bool skip = *flag != 0;
+  __syncthreads();
+  return skip;
+}
+
+// Large-cloud on-chip radix: one CTA sorts NP = NT * E points with only the
+// keys in registers; the 16-bit storage indices stay in shared memory
+// (double-buffered, moved by the scatter), so E = 16 fits the 64-register
+// budget of a 1024-thread CTA (the register-resident form spills there).
+// CS == 2: each CTA of a 2-CTA cluster sorts its half of the cloud, then both
+// merge the two sorted halves (merge path on the unique (key, index) pairs,
+// the partner's half read through DSMEM) and each writes NP outputs.
+// Clouds up to 65536 points (16-bit indices).
+template <int NT, int E, int CS, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    radix_cta_kernel(const float* __restrict__ xyz, long long N, int axis,
+                     float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+  constexpr int NW = NT / 32, NP = NT * E;
+  static_assert(CS == 1 || CS == 2, "one CTA or a pair");
+  static_assert(NP * CS <= 65536, "16-bit indices");
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* kb = smem;                                      // NP keys (exchange, then sorted)
+  uint16_t* ib = reinterpret_cast<uint16_t*>(smem + NP);    // [2][NP] indices
+  uint32_t* hist = smem + NP + NP;                          // [NW][256]
+  uint32_t* wsum = hist + 256 * NW;                         // [NW]
+  __shared__ int identity;
+  const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  const long long b = blockIdx.x / CS;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint32_t* hw = hist + w * 256;
+  const float* src = xyz + b * N * 3;
+  const int lb = w * 32 * E + lane;  // this thread's first slot (striped)
+  const long long gbase = static_cast<long long>(rank) * NP;
+
+  uint32_t key[E], rk[E / 2];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const long long g = gbase + lb + 32 * e;
+    key[e] = g < N ? order_key(__ldg(src + 3 * g + axis)) : 0xffffffffu;
+    ib[lb + 32 * e] = static_cast<uint16_t>(g);
+  }
+  int cur = 0;
+  for (int shift = 0; shift < 32; shift += 8) {
+    for (int i = t; i < 256 * NW; i += NT) hist[i] = 0;
+    if (t == 0) identity = 0;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t d = (key[e] >> shift) & 255u;
+      const unsigned peers = digit_peers(d);
+      const uint32_t before = hw[d];
+      __syncwarp();
+      if ((peers & lt_mask) == 0) hw[d] = before + __popc(peers);
+      __syncwarp();
+      const uint32_t r = before + __popc(peers & lt_mask);
+      if (e & 1) rk[e >> 1] |= r << 16; else rk[e >> 1] = r;
+    }
+    __syncthreads();
+    if (cta_digit_offsets<NT>(hist, wsum, &identity, NP)) continue;
+    const uint16_t* isrc = ib + cur * NP;
+    uint16_t* idst = ib + (cur ^ 1) * NP;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t dd = (key[e] >> shift) & 255u;
+      const uint32_t r = (e & 1) ? rk[e >> 1] >> 16 : rk[e >> 1] & 0xffffu;
+      const uint32_t pos = hw[dd] + r;
+      kb[pos] = key[e];
+      idst[pos] = isrc[lb + 32 * e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) key[e] = kb[lb + 32 * e];
+    cur ^= 1;
+  }
+  const uint16_t* is = ib + cur * NP;
+  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+  if constexpr (CS == 1) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const long long g = lb + 32 * e;
+      if (g < N) {
+        const int from = is[lb + 32 * e];
+        if (out_perm) out_perm[b * N + g] = from;
+        if (dst) gather_point(src, dst, g, from);
+      }
+    }
+  } else {
+    // The halves hold storage indices [0, NP) and [NP, 2 NP): on equal keys
+    // the first half's point comes first, so the merge compares keys only
+    // (A wins ties). Each CTA copies the partner's sorted keys next to its
+    // own (coalesced DSMEM reads), merges locally, then fetches the chosen
+    // indices (the partner's through DSMEM, all loads independent).
+    __shared__ int cur_sh;
+    uint32_t* kp = hist + 256 * NW + NW;  // NP partner keys
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) kb[lb + 32 * e] = key[e];
+    if (t == 0) cur_sh = cur;
+    cg::this_cluster().sync();
+    const int other = rank ^ 1;
+    const uint4* rk4 = reinterpret_cast<const uint4*>(cg::this_cluster().map_shared_rank(kb, other));
+    for (int i = t; i < NP / 4; i += NT) reinterpret_cast<uint4*>(kp)[i] = rk4[i];
+    const int ocur = *cg::this_cluster().map_shared_rank(&cur_sh, other);
+    const uint16_t* iown = ib + cur * NP;
+    const uint16_t* ioth = cg::this_cluster().map_shared_rank(ib, other) + ocur * NP;
+    const uint32_t* KA = rank == 0 ? kb : kp;
+    const uint32_t* KZ = rank == 0 ? kp : kb;
+    __syncthreads();
+    const int dg = rank * NP + t * E;  // this thread's E outputs (blocked)
+    int lo = dg > NP ? dg - NP : 0, hi = dg < NP ? dg : NP;
+    while (lo < hi) {  // first i with A[i] after Z[dg - i - 1]
+      const int mid = (lo + hi) >> 1;
+      if (KA[mid] <= KZ[dg - mid - 1]) lo = mid + 1; else hi = mid;
+    }
+    int i = lo, j = dg - lo;
+    uint32_t from[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool take_a = j >= NP || (i < NP && KA[i] <= KZ[j]);
+      from[e] = take_a ? static_cast<uint32_t>(i) : (0x10000u | static_cast<uint32_t>(j));
+      if (take_a) ++i; else ++j;
+    }
+    const uint16_t* IA = rank == 0 ? iown : ioth;
+    const uint16_t* IZ = rank == 0 ? ioth : iown;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      from[e] = (from[e] & 0x10000u) ? IZ[from[e] & 0xffffu] : IA[from[e]];
+    cg::this_cluster().sync();  // both CTAs done reading each other: reuse kb as staging
+#pragma unroll
+    for (int e = 0; e < E; ++e) kb[t * E + e] = from[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int p = lb + 32 * e;
+      const long long g = gbase + p;
+      if (g < N) {
+        const int f = static_cast<int>(kb[p]);
+        if (out_perm) out_perm[b * N + g] = f;
+        if (dst) gather_point(src, dst, g, f);
+      }
+    }
+  }
+}
+
+template <int NT, int E, int CS = 1, int MINB = 1>
+cudaError_t launch_radix_cta(const float* xyz, long long batch, long long n, int axis,
+                             float* out_xyz, int* out_perm, cudaStream_t st) {
+  constexpr int NW = NT / 32;
+  // keys, [2] 16-bit indices, per-warp digit counts, warp sums (+ the
+  // partner's keys for the 2-CTA merge)
+  const size_t smem = sizeof(uint32_t) * (2 * NT * E + 256 * NW + NW + (CS > 1 ? NT * E : 0));
+  auto kern = radix_cta_kernel<NT, E, CS, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(batch * CS));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace pcsk
 
 namespace pcs_internal {
@@ -1036,6 +1250,15 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     if (n <= 16384) return pcsk::launch_radix_reg<512, 8, 4, 2>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 32768) return pcsk::launch_radix_reg<512, 8, 8, 2>(x, batch, n, axis, o, out_perm, stream);
     return pcsk::launch_radix_reg<512, 8, 16, 2>(x, batch, n, axis, o, out_perm, stream);
+  }
+  // a wave or more of large clouds: one 16K-point CTA per cloud (or a pair
+  // merging their halves), indices in shared memory (radix_cta_kernel)
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && batch >= 148 && n <= 32768) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    if (n <= 8192) return pcsk::launch_radix_cta<512, 16, 1, 2>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 16384) return pcsk::launch_radix_cta<1024, 16, 1, 1>(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_radix_cta<1024, 16, 2, 1>(x, batch, n, axis, o, out_perm, stream);
   }
   if (coord_dtype == PCS_DTYPE_F32 && n > 1024 && n <= 16384) {
     const float* x = static_cast<const float*>(xyz);

@@ -206,7 +206,9 @@ def test_sort_parity(pcs):
 @pytest.mark.parametrize("radix", ["1", "0"])
 def test_sort_kernel_families(pcs, monkeypatch, radix):
     """Every on-chip sort variant (radix_reg_kernel: one CTA, clusters of
-    2K- and 4K-point CTAs; PCS_SORT_RADIX=0 forces the bitonic networks)
+    2K- and 4K-point CTAs; radix_cta_kernel: one 16K-point CTA per cloud or
+    a merging pair, for a wave of clouds; PCS_SORT_RADIX=0 forces the bitonic
+    networks)
     against numpy's stable argsort: ties, signed zeros, infinities, a
     constant axis (identity passes), ragged sizes."""
     import torch
@@ -215,21 +217,22 @@ def test_sort_kernel_families(pcs, monkeypatch, radix):
 
     monkeypatch.setenv("PCS_SORT_RADIX", radix)
     rng = np.random.default_rng(29)
-    for n in (3, 1024, 1500, 2048, 4096, 4097, 8192, 12000, 16384, 30000, 32768, 40000, 65536):
-        for b in (1, 16, 37, 38):
-            if b * n > 40 * 65536:
-                continue
-            xyz = np.round(rng.normal(size=(b, n, 3)), 1).astype(np.float32)
-            xyz[:, ::9, 0] = -0.0
-            xyz[:, 4::9, 0] = 0.0
-            xyz[:, 2::97, 0] = np.inf
-            xyz[:, 3::89, 0] = -np.inf
-            xyz[:, :, 1] = 0.5
-            for axis in (0, 1):
-                out, perm = sort_axis(torch.from_numpy(xyz).cuda(), axis)
-                want, order = synth.stable_sort_np(xyz, axis)
-                np.testing.assert_array_equal(perm.cpu().numpy(), order, err_msg=f"{b}x{n} ax{axis}")
-                np.testing.assert_array_equal(out.cpu().numpy(), want)
+    cases = [(b, n) for n in (3, 1024, 1500, 2048, 4096, 4097, 8192, 12000, 16384, 30000, 32768,
+                              40000, 65536) for b in (1, 16, 37, 38) if b * n <= 40 * 65536]
+    # a wave of clouds (>= 148): one CTA per cloud, or a pair merging halves
+    cases += [(150, n) for n in (5000, 8192, 12000, 16384, 20000, 32768)]
+    for b, n in cases:
+        xyz = np.round(rng.normal(size=(b, n, 3)), 1).astype(np.float32)
+        xyz[:, ::9, 0] = -0.0
+        xyz[:, 4::9, 0] = 0.0
+        xyz[:, 2::97, 0] = np.inf
+        xyz[:, 3::89, 0] = -np.inf
+        xyz[:, :, 1] = 0.5
+        for axis in (0, 1):
+            out, perm = sort_axis(torch.from_numpy(xyz).cuda(), axis)
+            want, order = synth.stable_sort_np(xyz, axis)
+            np.testing.assert_array_equal(perm.cpu().numpy(), order, err_msg=f"{b}x{n} ax{axis}")
+            np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
 def test_device_wide_radix_sort(pcs):

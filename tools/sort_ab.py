@@ -49,18 +49,20 @@ def timeit(x, reps=10):
 
 
 rng = np.random.default_rng(0)
-for n in () if os.environ.get("SORT_AB_SKIP_PARITY") else (1, 2, 31, 100, 1000, 1024, 1025, 2048, 3000, 4096, 5000, 8192, 8193, 12000, 16384,
-          20000, 32768, 50000, 65536, 100000, 131072):
-  for cfg in ("a", "b"):
-    os.environ["PCS_RADIX_CFG"] = cfg
-    for b in (1, 3):
+SIZES = (1, 2, 31, 100, 1000, 1024, 1025, 2048, 3000, 4096, 5000, 8192, 8193, 12000, 16384,
+         20000, 32768, 50000, 65536, 100000, 131072)
+for n in () if os.environ.get("SORT_AB_SKIP_PARITY") else SIZES:
+    for b in (1, 3, 150):  # 150 clouds: the one-wave radix_cta path
+        if b * n > 150 * 40000:
+            continue
         x = rng.standard_normal((b, n, 3)).astype(np.float32)
         x[:, ::7, 0] = np.round(x[:, ::7, 0], 1)       # ties
         x[:, ::11, 0] = 0.0
         x[:, ::13, 0] = -0.0                            # -0 == +0, storage order
         x[:, ::17, 0] = -x[:, ::17, 0]
         if n > 5:
-            x[:, 3, 0] = np.inf; x[:, 4, 0] = -np.inf
+            x[:, 3, 0] = np.inf
+            x[:, 4, 0] = -np.inf
         check(x)
         check(x, 2)
     xs = np.ones((1, n, 3), np.float32)                 # one key: identity passes
@@ -69,18 +71,17 @@ print("parity ok", flush=True)
 CASES = [(16, 2048), (64, 8192), (256, 2048), (256, 4096), (256, 8192), (256, 16384),
          (256, 32768), (1, 2048), (4, 32768), (8, 131072)]
 if os.environ.get("SORT_AB_GRID"):
-    CASES = [(b, n) for n in (8192, 16384, 32768, 65536) for b in (1, 4, 16, 37, 64, 148)]
+    CASES = [(b, n) for n in (8192, 16384, 32768) for b in (64, 100, 148, 200, 296)]
 if os.environ.get("SORT_AB_SKIP_PARITY"):
     pass
 for B, N in CASES:
     x = synth.uniform_cube(B, N, 1)
-    os.environ["PCS_SORT_RADIX"] = "0"
-    t0 = timeit(x)
-    os.environ["PCS_SORT_RADIX"] = "1"
-    res = []
-    for cfg in ("a", "b"):
-        os.environ["PCS_RADIX_CFG"] = cfg
-        res.append(timeit(x))
+    res = {}
+    for arm, env in (("bitonic", {"PCS_SORT_RADIX": "0"}), ("dispatch", {})):
+        os.environ.pop("PCS_SORT_RADIX", None)
+        os.environ.update(env)
+        res[arm] = timeit(x)
+    os.environ.pop("PCS_SORT_RADIX", None)
     gb = B * N * 28 / 1e9
-    print(f"{B}x{N}: bitonic {t0:.4f} ms  radix a {res[0]:.4f} b {res[1]:.4f} ms "
-          f"({gb / min(res) * 1e3:.0f} GB/s alg)", flush=True)
+    print(f"{B}x{N}: " + "  ".join(f"{k} {v:.4f}" for k, v in res.items()) +
+          f" ms ({gb / min(res.values()) * 1e3:.0f} GB/s alg)", flush=True)
