@@ -159,7 +159,27 @@ struct DevStreams {
   cudaStream_t copy = nullptr, work[kWorkers] = {};
   cudaEvent_t ev[kEvents] = {};
   bool ok = false;
+  // pinned host staging for the per-cloud drop-in entries (grown on demand,
+  // used under `mu`): copies from pinned memory are true async DMA, while a
+  // pageable source goes through the driver's bounce buffers
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
+
+// The caller holds ds.mu; previous users of the buffer have synchronised.
+cudaError_t pinned_scratch(DevStreams& ds, size_t bytes, void** out) {
+  if (bytes > ds.pinned_bytes) {
+    if (ds.pinned) cudaFreeHost(ds.pinned);
+    ds.pinned = nullptr;
+    ds.pinned_bytes = 0;
+    const size_t want = std::max(bytes, size_t(1) << 20);
+    const cudaError_t e = cudaHostAlloc(&ds.pinned, want, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    ds.pinned_bytes = want;
+  }
+  *out = ds.pinned;
+  return cudaSuccess;
+}
 
 cudaError_t device_streams(DevStreams** out) {
   static std::mutex init_mu;
@@ -301,21 +321,24 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
   // same, the copy is halved and large sectors get the tensor-memory Morton
   // engine. (Windowed samplers keep fp64 staging: one cloud's NPDU sectors
   // are latency-bound and fp64 coordinates need no per-iteration widening.)
-  std::vector<float> f32;
   const bool windowed = method == PCS_METHOD_NPDU_FPS || method == PCS_METHOD_NPDU_AFPS;
-  if (!windowed) {
-    bool exact = true;
-    for (int64_t i = 0; i < 3 * n && exact; ++i) {
-      const float f = static_cast<float>(xyz[i]);
-      exact = static_cast<double>(f) == xyz[i];  // NaN: not exact
-    }
-    if (exact) {
-      f32.resize(static_cast<size_t>(3 * n));
-      for (int64_t i = 0; i < 3 * n; ++i) f32[i] = static_cast<float>(xyz[i]);
-    }
+  bool use32 = !windowed;
+  for (int64_t i = 0; i < 3 * n && use32; ++i) {
+    const float f = static_cast<float>(xyz[i]);
+    use32 = static_cast<double>(f) == xyz[i];  // NaN: not exact
   }
-  const bool use32 = !f32.empty() || n == 0;
+  use32 = use32 || n == 0;
   const size_t coord_bytes = (use32 ? sizeof(float) : sizeof(double)) * 3 * n;
+  // the cloud (fp32 copy or the doubles) staged in pinned memory
+  void* stage = nullptr;
+  e = pinned_scratch(*dsp, coord_bytes, &stage);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (use32) {
+    float* f32 = static_cast<float*>(stage);
+    for (int64_t i = 0; i < 3 * n; ++i) f32[i] = static_cast<float>(xyz[i]);
+  } else {
+    std::memcpy(stage, xyz, coord_bytes);
+  }
   // one workspace: cloud, indices, sector ids (int32 on the device), stats
   const size_t b_xyz = (coord_bytes + 255) & ~size_t(255);
   const size_t b_idx = (sizeof(int64_t) * c + 255) & ~size_t(255);
@@ -327,8 +350,7 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
   int32_t* dsec = reinterpret_cast<int32_t*>(base + b_xyz + b_idx);
   uint64_t* dstat = reinterpret_cast<uint64_t*>(base + b_xyz + b_idx + b_sec);
   std::vector<int32_t> sec32(out_sector ? static_cast<size_t>(c) : 0);
-  e = cudaMemcpyAsync(base, use32 ? static_cast<const void*>(f32.data()) : static_cast<const void*>(xyz),
-                      coord_bytes, cudaMemcpyHostToDevice, st);
+  e = cudaMemcpyAsync(base, stage, coord_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     pcs_gpu_args a{};
     a.method = method;
@@ -412,6 +434,47 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
   std::lock_guard<std::mutex> lock(dsp->mu);
   cudaStream_t st = dsp->copy;
   int rc = PCS_OK;
+  // The order depends on the axis column alone. When every axis value is
+  // exactly representable in fp32 (clouds read from f32_bin files or float32
+  // arrays, forcecast to float64 by the binding), sort fp32 keys: the same
+  // operator< order (fp32 widens exactly; -0.0 folds onto +0.0 either way),
+  // a third of the copy, the on-chip fp32 sort kernels; only the permutation
+  // comes back and the host gathers the float64 points through it.
+  bool f32_keys = n <= 0x7fffffffLL;
+  for (int64_t i = 0; i < n && f32_keys; ++i) {
+    const double v = xyz[3 * i + axis];
+    f32_keys = static_cast<double>(static_cast<float>(v)) == v;  // NaN: not exact
+  }
+  if (f32_keys) {
+    DevBuf dk(st), dperm(st);
+    // pinned staging: the keys in column 0 of an (n, 3) fp32 array (the
+    // sort kernels' layout, sorted on axis 0), then the permutation
+    void* stage = nullptr;
+    if ((e = pinned_scratch(*dsp, sizeof(float) * 4 * n, &stage)) != cudaSuccess) return cuda_fail(e);
+    float* keys = static_cast<float*>(stage);
+    int32_t* perm32 = reinterpret_cast<int32_t*>(keys + 3 * n);
+    for (int64_t i = 0; i < n; ++i) keys[3 * i] = static_cast<float>(xyz[3 * i + axis]);
+    if ((e = dk.alloc(sizeof(float) * 3 * n)) != cudaSuccess ||
+        (e = dperm.alloc(sizeof(int32_t) * n)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dk.p, keys, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = launch_sort(PCS_DTYPE_F32, dk.p, 1, n, 0, nullptr, static_cast<int32_t*>(dperm.p), st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(perm32, dperm.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      rc = cuda_fail(e);
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t from = perm32[i];
+        if (out_perm) out_perm[i] = from;
+        if (out_xyz) {
+          out_xyz[3 * i] = xyz[3 * from];
+          out_xyz[3 * i + 1] = xyz[3 * from + 1];
+          out_xyz[3 * i + 2] = xyz[3 * from + 2];
+        }
+      }
+    }
+    cudaStreamSynchronize(st);
+    return rc;
+  }
   {
     DevBuf dx(st), dout(st), dperm(st);
     int32_t* perm32 = new int32_t[n];

@@ -1,12 +1,14 @@
 // Python module `paper_2208_08795_b200._core`: the reference's pcsample._core
 // sampler surface (proj/bindings/pcsample_module.cpp:122-190) -- same names,
 // keyword arguments, defaults, return types and exception classes -- plus raw
-// device-pointer entry points used by the torch batched op. Calls the C++
-// drop-in (include/pcs/*.hpp), which calls the C-ABI (include/pcs_gpu.h).
+// device-pointer entry points used by the torch batched op. The samplers and
+// exact_sort call the C-ABI host entries (include/pcs_gpu.h) on the numpy
+// buffer directly; the rest goes through the C++ drop-in (include/pcs/*.hpp).
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -71,21 +73,50 @@ py::tuple to_tuple(const pcs::SampleResult& r) {
   return py::make_tuple(idx, sec, stats);
 }
 
-template <typename Fn>
-py::tuple sample(const F64Array& points, Fn&& fn) {
-  const pcs::PointCloud cloud = to_cloud(points);
-  pcs::SampleResult r;
-  {
-    py::gil_scoped_release nogil;
-    r = fn(cloud);
-  }
-  return to_tuple(r);
-}
-
 void check(int rc) {
   if (rc == PCS_OK) return;
   if (rc == PCS_ERR_INVALID_ARGUMENT) throw std::invalid_argument(pcs_last_error());
   throw std::runtime_error(pcs_last_error());
+}
+
+const double* xyz_of(const F64Array& a, std::int64_t* n) {
+  const auto info = a.request();
+  if (info.ndim != 2 || info.shape[1] != 3) throw std::invalid_argument("expected an (N, 3) array");
+  *n = static_cast<std::int64_t>(info.shape[0]);
+  return static_cast<const double*>(info.ptr);
+}
+
+// The samplers straight through the C-ABI host entry on the (forcecast,
+// contiguous) array: the same validation order and messages as pcs::fps &
+// co. (both use the C-ABI's checks), without the PointCloud copy -- a
+// measurable share of a per-cloud call at 32K points.
+py::tuple sample(const F64Array& points, int method, std::size_t c, std::size_t mm, std::size_t k,
+                 pcs::SeedPolicy policy, std::uint64_t seed) {
+  std::int64_t n = 0;
+  const double* xyz = xyz_of(points, &n);
+  // results are written only when c is feasible (c <= n)
+  const auto cap = static_cast<py::ssize_t>(
+      std::max<std::size_t>(1, std::min<std::size_t>(c, static_cast<std::size_t>(n))));
+  py::array_t<std::int64_t> idx(cap), sec(cap);
+  std::int64_t* pi = idx.mutable_data();
+  std::int64_t* ps = sec.mutable_data();
+  std::uint64_t st[4] = {0, 0, 0, 0};
+  int rc;
+  {
+    py::gil_scoped_release nogil;
+    rc = pcs_sample_host(method, xyz, n, static_cast<std::int64_t>(c), static_cast<std::int64_t>(mm),
+                         static_cast<std::int64_t>(k),
+                         policy == pcs::SeedPolicy::RandomFirstPoint ? PCS_RANDOM_FIRST_POINT
+                                                                     : PCS_FIXED_FIRST_POINT,
+                         seed, 1, pi, ps, st);
+  }
+  check(rc);
+  py::dict stats;
+  stats["dist_evals"] = st[0];
+  stats["dist_writes"] = st[1];
+  stats["argmax_scans"] = st[2];
+  stats["iterations"] = st[3];
+  return py::make_tuple(idx, sec, stats);
 }
 
 }  // namespace
@@ -96,16 +127,15 @@ PYBIND11_MODULE(_core, m) {
   m.def("fps",
         [](const F64Array& points, std::size_t c, std::uint64_t seed, const std::string& first) {
           const auto policy = policy_of(first);
-          return sample(points, [&](const pcs::PointCloud& cl) { return pcs::fps(cl, c, policy, seed); });
+          return sample(points, PCS_METHOD_FPS, c, 1, 0, policy, seed);
         },
         py::arg("points"), py::arg("c"), py::arg("seed") = 0, py::arg("first") = "random");
   m.def("afps",
         [](const F64Array& points, std::size_t c, std::size_t mm, std::uint64_t seed,
            const std::string& first, unsigned threads) {
           const auto policy = policy_of(first);
-          return sample(points, [&](const pcs::PointCloud& cl) {
-            return pcs::afps(cl, c, mm, policy, seed, threads);
-          });
+          (void)threads;  // accepted for the reference signature; the GPU schedule is fixed
+          return sample(points, PCS_METHOD_AFPS, c, mm, 0, policy, seed);
         },
         py::arg("points"), py::arg("c"), py::arg("m"), py::arg("seed") = 0,
         py::arg("first") = "random", py::arg("threads") = 1);
@@ -113,7 +143,7 @@ PYBIND11_MODULE(_core, m) {
         [](const F64Array& points, std::size_t c, std::size_t k, std::uint64_t seed,
            const std::string& first) {
           const auto policy = policy_of(first);
-          return sample(points, [&](const pcs::PointCloud& cl) { return pcs::npdu_fps(cl, c, k, policy, seed); });
+          return sample(points, PCS_METHOD_NPDU_FPS, c, 1, k, policy, seed);
         },
         py::arg("points"), py::arg("c"), py::arg("k"), py::arg("seed") = 0,
         py::arg("first") = "random");
@@ -121,22 +151,25 @@ PYBIND11_MODULE(_core, m) {
         [](const F64Array& points, std::size_t c, std::size_t mm, std::size_t k, std::uint64_t seed,
            const std::string& first, unsigned threads) {
           const auto policy = policy_of(first);
-          return sample(points, [&](const pcs::PointCloud& cl) {
-            return pcs::npdu_afps(cl, c, mm, k, policy, seed, threads);
-          });
+          (void)threads;
+          return sample(points, PCS_METHOD_NPDU_AFPS, c, mm, k, policy, seed);
         },
         py::arg("points"), py::arg("c"), py::arg("m"), py::arg("k"), py::arg("seed") = 0,
         py::arg("first") = "random", py::arg("threads") = 1);
   m.def("exact_sort",
         [](const F64Array& points, const std::string& axis) {
           const auto ax = axis_of(axis);
-          const pcs::PointCloud cloud = to_cloud(points);
-          pcs::PointCloud sorted;
-          {
+          std::int64_t n = 0;
+          const double* xyz = xyz_of(points, &n);
+          py::array_t<double> out({static_cast<py::ssize_t>(n), py::ssize_t{3}});
+          double* dst = out.mutable_data();
+          int rc = PCS_OK;
+          if (n > 0) {
             py::gil_scoped_release nogil;
-            sorted = pcs::exact_sort(cloud, ax);
+            rc = pcs_exact_sort_host(xyz, n, static_cast<int>(ax), dst, nullptr);
           }
-          return to_array(sorted);
+          check(rc);
+          return out;
         },
         py::arg("points"), py::arg("axis") = "x");
   m.def("local_fps",

@@ -235,6 +235,31 @@ def test_sort_kernel_families(pcs, monkeypatch, radix):
             np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
+def test_exact_sort_dropin_fp32_keys(pcs):
+    """pcs.exact_sort on float64 clouds whose axis column is fp32-exact sorts
+    fp32 keys on the device and gathers the float64 points on the host: the
+    other columns keep full double precision, ties keep storage order, -0.0
+    equals +0.0; a column with one non-fp32 value takes the fp64 path."""
+    rng = np.random.default_rng(31)
+    for n in (1, 2, 100, 2048, 5000, 32768, 70000, 300000):
+        pts = rng.normal(size=(n, 3))                      # full-precision doubles
+        col = np.round(rng.normal(size=n), 2).astype(np.float32).astype(np.float64)
+        col[::13] = -0.0
+        col[1::13] = 0.0
+        if n > 10:
+            col[5] = np.inf
+            col[6] = -np.inf
+        for axis in (0, 2):
+            p = pts.copy()
+            p[:, axis] = col
+            want = synth.stable_sort_np(p[None], axis)[0][0]
+            np.testing.assert_array_equal(pcs.exact_sort(p, "xyz"[axis]), want, err_msg=f"{n}")
+            if n > 10:
+                p[7, axis] = 0.1  # not representable in fp32
+                want = synth.stable_sort_np(p[None], axis)[0][0]
+                np.testing.assert_array_equal(pcs.exact_sort(p, "xyz"[axis]), want)
+
+
 def test_device_wide_radix_sort(pcs):
     """Clouds past one CTA / one cluster: the multi-CTA LSD radix (fp32 >
     256K points, fp64 >= 64K), stable with ties and signed zeros, batched."""

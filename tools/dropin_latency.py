@@ -30,3 +30,13 @@ for n, c in ((8192, 2048), (32768, 1024)):
         pcs.fps(pts, c)
         ts.append((time.perf_counter() - t0) * 1e3)
     print("fps", n, c, "ms/call median %.3f" % float(np.median(ts)))
+for n in (2048, 8192, 32768, 131072):
+    pts = synth.uniform_cube(1, n, 3)[0].astype(np.float64)
+    for _ in range(3):
+        pcs.exact_sort(pts, "x")
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        pcs.exact_sort(pts, "x")
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print("exact_sort", n, "ms/call median %.3f" % float(np.median(ts)))
