@@ -100,6 +100,12 @@ def build(verbose=False):
               "-I", pybind11.get_include(), "-I", sysconfig.get_paths()["include"],
               mod_src, "-o", core, "-L", LIBDIR, "-lpcs_gpu", "-Wl,-rpath,$ORIGIN/lib"],
              verbose)
+    # the C++ drop-in API test (tests/cpp, run by the GPU suite)
+    test_src = os.path.join(ROOT, "tests", "cpp", "test_pcs_api.cpp")
+    test_bin = os.path.join(OBJDIR, "test_pcs_api")
+    if os.path.exists(test_src) and _newer(test_bin, [test_src, LIB] + hdrs):
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", INC, test_src, "-o", test_bin,
+              "-L", LIBDIR, "-lpcs_gpu", "-Wl,-rpath,$ORIGIN/../lib"], verbose)
     return LIB, core
 
 

@@ -754,3 +754,16 @@ def test_cuda_graph_capture_and_replay():
     torch.cuda.synchronize()
     for a, b in zip(want, out):
         assert torch.equal(a, b)
+
+
+def test_cpp_dropin_api_kats():
+    """The C++ drop-in (include/pcs/*.hpp) against the reference's unit-test
+    known answers: tests/cpp/test_pcs_api.cpp, built by _build.py."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2208_08795_b200", "build", "test_pcs_api")
+    assert os.path.exists(exe), "run __graft_entry__.build() first"
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "all checks passed" in p.stdout
