@@ -562,9 +562,17 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   // warps per CTA (one CTA per SM): TMEM holds 4 lane quarters x (512 / cpw)
   // column blocks; shared memory and 32 warps bound it too
   long long G = std::min<long long>({32, 4LL * (512 / cpw), static_cast<long long>(kMaxSmem / wsm)});
-  // balance the waves: as many CTAs per wave as SMs, the same warps in each
+  // One wave: balance it (as many CTAs as SMs, the same warps in each).
+  // More than one: CTAs of 4 warps (one TMEM column block) -- several per SM,
+  // replaced as they finish, so the SMs stay near full occupancy without a
+  // wave tail (cfg4 0.404 -> 0.386 ms, 256x32K M=16 1.01 -> 0.93 ms; one-wave
+  // batches keep the balanced single CTA: 256x4K 0.065 vs 0.10 ms).
   const long long waves = (sectors + 148 * G - 1) / (148 * G);
-  G = std::max(1LL, std::min(G, (sectors + 148 * waves - 1) / (148 * waves)));
+  if (waves >= 2 && G >= 4)
+    G = 4;
+  else
+    G = std::max(1LL, std::min(G, (sectors + 148 * waves - 1) / (148 * waves)));
+  if (const char* ge = std::getenv("PCS_NPDU_G")) G = std::max(1, std::atoi(ge));  // A/B knob
   int cols = 32;
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
