@@ -208,6 +208,15 @@ def host_sorted(w, xyz):
     return synth.stable_sort_np(xyz, "xyz".index(w["sort"]))[0]
 
 
+def arm_config(workload, w, world, strong):
+    """The `config` object both arms print (identical for the same workload)."""
+    return {"workload": workload, "clouds_per_gpu": w["B"], "points_per_cloud": w["N"],
+            "samples_per_cloud": w["C"], "method": w["method"], "m": w["M"], "k": w["K"],
+            "sort": w["sort"], "generator": w["gen"], "coords": "fp32 in, fp64 math",
+            "l2": "flushed between steps (512 MiB write)",
+            "parallelism": (f"sector-split x{world}" if strong else f"dp{world}")}
+
+
 def run_reference_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -218,7 +227,8 @@ def run_reference_arm(args, w):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, **{k: v for k, v in w.items()}},
+            "config": arm_config(args.workload, w, args.gpus,
+                                 bool(w.get("strong")) and args.gpus > 1),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "clouds_per_s": res["clouds_per_s"], "cpu_model": res["cpu_model"],
             "e2e": {"value": res["value"], "unit": "sampled points/s",
@@ -416,11 +426,7 @@ def main():
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "clouds_per_s": (B if strong else world * B) / (ms_per_step * 1e-3),
-            "config": {"workload": args.workload, "clouds_per_gpu": B, "points_per_cloud": N,
-                       "samples_per_cloud": C, "method": w["method"], "m": w["M"], "k": w["K"],
-                       "sort": w["sort"], "generator": w["gen"], "coords": "fp32 in, fp64 math",
-                       "l2": "flushed between steps (512 MiB write)",
-                       "parallelism": (f"sector-split x{world}" if strong else f"dp{world}")},
+            "config": arm_config(args.workload, w, world, strong),
             "gpu_launches": args.steps * launches_per_step(w),
             "dist_evals_per_step": evals_per_step,
             "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
