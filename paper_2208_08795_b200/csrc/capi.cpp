@@ -220,8 +220,16 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
   const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
-  int nch = chunks > 0 ? chunks : 8;
-  if (nch > B) nch = static_cast<int>(B);
+  // Chunk boundaries: `chunks` (<= 0: 8) equal chunks. (Splitting the last
+  // chunk s/2, s/4, s/4 so its sectors take the lower-latency W-warp NPDU
+  // kernel measured slower: cfg4 e2e 1.14 -> 1.22 ms, the small chunks'
+  // kernels overlap on the worker streams.)
+  std::vector<int64_t> bounds{0};
+  {
+    const int64_t nu = std::min<int64_t>(std::min<int64_t>(B, chunks > 0 ? chunks : 8), kEvents - 4);
+    for (int64_t i = 1; i <= nu; ++i) bounds.push_back(B * i / nu);
+  }
+  int nch = static_cast<int>(bounds.size()) - 1;
   DevStreams* dsp = nullptr;
   cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -229,7 +237,6 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   DevStreams& ds = *dsp;
   cudaStream_t copy = ds.copy;
   cudaStream_t* work = ds.work;
-  if (nch > kEvents - 1) nch = kEvents - 1;
   void* ws = nullptr;
   size_t off_xyz = 0, off_srt = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
   if (e == cudaSuccess) {
@@ -250,7 +257,7 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   cudaEvent_t seeds_ready = ds.ev[kEvents - 1];  // the workspace (and seeds) exist
   if (e == cudaSuccess) e = cudaEventRecord(seeds_ready, copy);
   for (int i = 0; i < nch && e == cudaSuccess; ++i) {
-    const int64_t b0 = B * i / nch, b1 = B * (i + 1) / nch, nb = b1 - b0;
+    const int64_t b0 = bounds[i], b1 = bounds[i + 1], nb = b1 - b0;
     if (nb == 0) continue;
     cudaStream_t w = work[i % kWorkers];
     char* dx = base + off_xyz + cloud_bytes * b0;

@@ -130,6 +130,126 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
   flush_stats<W>(p, gs, t, writes, evals);
 }
 
+// ------------------------------------------------------ window, latency form
+// NPDU sectors when the SMs hold few of them (the per-iteration chain, not
+// issue, is the limit there). The full kernel's layout -- W warps per sector,
+// point j = k*T + t in registers, so row r (32 points) belongs to warp r % W,
+// slot r / W -- but each iteration evaluates only the slots whose row meets
+// update_window [wb, we) (sectors.cpp:53-61): a window of R rows spreads over
+// min(R, W) warps that work in parallel, and the per-thread max over P slots
+// plus the group argmax replace the one-warp kernel's per-row key cache.
+template <int P, int W>
+__global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
+    npdu_wide_kernel(const SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int T = W * 32;
+  const int gid = threadIdx.x / T, t = threadIdx.x % T, lane = t & 31, warp = t >> 5;
+  GroupSetup gs;
+  if (!setup_group<W>(p, smem, gid, t, gs)) return;
+  const int n = gs.g.n;
+  group_sync<W>(gid);
+
+  double x[P], y[P], z[P], d[P];
+  unsigned vmask = 0;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int j = k * T + t;
+    const bool valid = j < n;
+    vmask |= valid ? (1u << k) : 0u;
+    const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+    x[k] = valid ? gs.xs[j] : kNaN;
+    y[k] = valid ? gs.ys[j] : kNaN;
+    z[k] = valid ? gs.zs[j] : kNaN;
+    d[k] = valid ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+  }
+
+  int cur = first_point(p, gs);
+  const long long obase = gs.b * p.C + gs.g.out_off;
+  const long long ioff = gs.g.begin + p.index_base;
+  const bool idx64 = p.idx64 != 0;
+  void* const out = p.out_idx;
+  int ob = cur;
+  auto flush = [&](int i0, int cnt) {
+    if (warp == 0 && lane < cnt) {
+      if (idx64) static_cast<long long*>(out)[obase + i0 + lane] = ioff + ob;
+      else static_cast<int*>(out)[obase + i0 + lane] = static_cast<int>(ioff + ob);
+    }
+  };
+  unsigned smask = (cur % T == t) ? (1u << (cur / T)) : 0u;
+  double* const trace = p.trace;
+  const int half_down = static_cast<int>(p.K / 2), half_up = static_cast<int>((p.K + 1) / 2);
+  unsigned writes = 0;
+  unsigned long long evals = 0;
+  int round = 0;
+#ifdef PCS_PROF
+  unsigned long long pacc[5] = {0, 0, 0, 0, 0};
+#endif
+  for (int it = 1; it < gs.g.quota; ++it) {
+    FPROF_T(t0);
+    const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
+    const int wb = cur >= half_down ? cur - half_down : 0;
+    const int we = min(n, cur + half_up);
+    evals += static_cast<unsigned long long>(we - wb);
+    const int r_lo = wb >> 5, r_hi = (we - 1) >> 5;
+    unsigned long long best = 0;
+    int bs = -1;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int r = k * W + warp;
+      if (r >= r_lo && r <= r_hi) {  // warp-uniform: this slot's row meets the window
+        const int j = k * T + t;
+        const double dist = dist2(x[k], y[k], z[k], px, py, pz);
+        const bool lower = j >= wb && j < we && dist <= d[k];
+        writes += lower ? 1u : 0u;
+        d[k] = lower ? dist : d[k];
+      }
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+      if (bits > best) {
+        best = bits;
+        bs = k;
+      }
+    }
+    if (trace) {
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        if ((vmask >> k) & 1u) trace[static_cast<long long>(it - 1) * n + k * T + t] = d[k];
+    }
+    uint32_t hi = static_cast<uint32_t>(best >> 32), lo = static_cast<uint32_t>(best);
+    uint32_t j = bs >= 0 ? static_cast<uint32_t>(bs * T + t) : kNoIndex;
+#ifdef PCS_PROF
+    FPROF_T(t1);
+    warp_argmax(hi, lo, j);
+    FPROF_T(t2);
+    {
+      uint4* buf = gs.cand + (round & 1) * W;
+      if (lane == 0) buf[warp] = make_uint4(hi, lo, j, 0);
+      named_bar_sync(1 + gid, W * 32);
+      const uint4 v = lane < W ? buf[lane] : make_uint4(0, 0, kNoIndex, 0);
+      hi = v.x; lo = v.y; j = v.z;
+    }
+    FPROF_T(t3);
+    warp_argmax(hi, lo, j);
+    ++round;
+    FPROF_T(t4);
+    pacc[0] += t1 - t0; pacc[1] += t2 - t1; pacc[2] += t3 - t2; pacc[3] += t4 - t3; pacc[4] += 1;
+#else
+    group_argmax<W>(hi, lo, j, gs.cand, round, gid, lane, warp);
+#endif
+    if ((hi | lo) == 0u)
+      j = lowest_unsampled<P, W>(vmask, smask, t, gs.cand, round, gid, lane, warp);
+    cur = static_cast<int>(j);
+    if (lane == (it & 31)) ob = cur;
+    if ((it & 31) == 31) flush(it - 31, 32);
+    if (cur % T == t) smask |= 1u << (cur / T);
+  }
+#ifdef PCS_PROF
+  if (t == 0)
+    for (int q = 0; q < 5; ++q) atomicAdd(&g_fprof[q], pacc[q]);
+#endif
+  if (((gs.g.quota - 1) & 31) != 31) flush((gs.g.quota - 1) & ~31, ((gs.g.quota - 1) & 31) + 1);
+  flush_stats<W>(p, gs, t, writes, evals);
+}
+
 template <typename Kern>
 cudaError_t launch_groups(Kern kern, SampleParams p, int W, int G, cudaStream_t st) {
   const size_t group_bytes = size_t(24) * p.nmax + 32 * W;
@@ -192,6 +312,25 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   if (n <= 1024) return run_full<16, 2, true>(p, st);
   if (n <= 2048) return run_full<16, 4, true>(p, st);
   if (n <= 4096) return run_full<16, 8, true>(p, st);
+  return cudaErrorNotSupported;
+}
+
+template <int P, int W>
+cudaError_t run_wide(SampleParams p, cudaStream_t st) {
+  const int G = pick_groups(p.B * p.M, W, p.nmax, W >= 8 ? W * 32 : 256);
+  return launch_groups(npdu_wide_kernel<P, W>, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
+}
+
+// Windowed sectors <= 4096 points, W >= 8 warps (a window of <= 8 rows -- k
+// <= 225 -- then meets at most one row per warp).
+cudaError_t run_npdu_wide_any(SampleParams p, long long n, cudaStream_t st) {
+  // (8 warps measured best: 1024-point sectors at 1 per SM, 16 warps x 2
+  // slots 0.148 ms, 32 x 1 0.213 ms, 8 x 4 0.117 ms; one warp 0.142 ms)
+  if (n <= 256) return run_wide<1, 8>(p, st);
+  if (n <= 512) return run_wide<2, 8>(p, st);
+  if (n <= 1024) return run_wide<4, 8>(p, st);
+  if (n <= 2048) return run_wide<8, 8>(p, st);
+  if (n <= 4096) return run_wide<8, 16>(p, st);
   return cudaErrorNotSupported;
 }
 

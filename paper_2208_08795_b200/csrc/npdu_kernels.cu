@@ -588,6 +588,16 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
 }
 
 cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
+  // At most one sector per SM: the serial update -> argmax chain is the
+  // limit, and the W-warp register kernel (full_kernels.cu) runs it ~18%
+  // shorter than one warp per sector. PCS_NPDU_WIDE = the largest batch (in sectors) that
+  // takes it (0 disables).
+  long long wide_max = kNpduWideMax;
+  if (const char* wv = std::getenv("PCS_NPDU_WIDE")) wide_max = std::atoll(wv);
+  if (p.B * p.M <= wide_max && n <= 4096) {
+    const cudaError_t e = run_npdu_wide_any(p, n, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const char* tmv = std::getenv("PCS_NPDU_TMEM");
   const bool use_tmem = !(tmv && tmv[0] == '0');
   const long long rows_needed = (p.K + 62) / 32;

@@ -201,11 +201,17 @@ __device__ __forceinline__ uint32_t lowest_unsampled(unsigned vmask, unsigned sm
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
+// windowed batches of at most this many sectors (one per SM) take
+// npdu_wide_kernel: cfg4 sectors (1024 points, k=129) at 32-128 sectors
+// 0.117 vs 0.142 ms; at 256 sectors the one-warp TMEM kernel wins again
+// (0.141 vs 0.152 ms) and at 512 by 2x (tools/npdu_wide_ab.py)
+constexpr long long kNpduWideMax = 148;
 
 // Launchers (one per translation unit). They return cudaErrorNotSupported
 // when the sector does not fit the kernel family.
 cudaError_t run_full_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_npdu_any(SampleParams p, long long nmax_sector, cudaStream_t st);
+cudaError_t run_npdu_wide_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_rows_any(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st);
 cudaError_t run_morton_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_morton_tmem_any(SampleParams p, long long nmax_sector, cudaStream_t st);

@@ -217,6 +217,10 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
     if rows:
         return "rows_kernel"
     if windowed:
+        # few sectors: the W-warp latency form (csrc/npdu_kernels.cu, kNpduWideMax)
+        if nmax <= 4096 and batch * (m if sectored else 1) <= \
+                int(os.environ.get("PCS_NPDU_WIDE", "148")):
+            return "npdu_wide_kernel"
         if nmax <= 4096 and (k + 62) // 32 <= 5 and dtype != "float64" and \
                 os.environ.get("PCS_NPDU_TMEM", "1") != "0":
             return "npdu_tmem_kernel"

@@ -19,6 +19,15 @@ pytestmark = pytest.mark.gpu
 LINE = np.array([[float(x), 0.0, 0.0] for x in range(8)])
 
 
+@pytest.fixture(params=["wide", "one_warp"])
+def npdu_engine(request, monkeypatch):
+    """NPDU sectors <= 4096 points run on the W-warp latency form
+    (npdu_wide_kernel) for small batches and on the one-warp TMEM / shared-
+    memory kernels otherwise: force each (PCS_NPDU_WIDE = max sectors)."""
+    monkeypatch.setenv("PCS_NPDU_WIDE", "100000000" if request.param == "wide" else "0")
+    return request.param
+
+
 def _call(pcs, meth, pts, c, m, k, first, seed):
     if meth == "fps":
         return pcs.fps(pts, c, seed=seed, first=first)
@@ -70,7 +79,7 @@ def test_reference_kats(pcs):
     assert a[0].tolist() == r[0].tolist() and a[2] == r[2]
 
 
-def test_reduction_identities(pcs):
+def test_reduction_identities(pcs, npdu_engine):
     # proj/tests/acceptance_main.cpp:128-171
     rng = np.random.default_rng(260856)
     for trial in range(25):
@@ -95,7 +104,7 @@ def test_reduction_identities(pcs):
         assert wa[0].tolist() == a[0].tolist() and wa[2] == a[2]
 
 
-def test_random_configs_vs_oracle(pcs, oracle):
+def test_random_configs_vs_oracle(pcs, oracle, npdu_engine):
     rng = np.random.default_rng(7777)
     for t in range(160):
         n = int(rng.integers(4, 3000 if t % 8 else 8193))
@@ -114,7 +123,7 @@ def test_random_configs_vs_oracle(pcs, oracle):
         _same(got, *want)
 
 
-def test_distance_trace_bit_exact(pcs, oracle):
+def test_distance_trace_bit_exact(pcs, oracle, npdu_engine):
     pts = synth.random_cloud(300, 404)
     for k in (None, 7):
         idx, _, st, tr = pcs.local_fps(pts, 40, 290, 60, k=k, seed=3, first="random", trace=True)
@@ -139,7 +148,7 @@ def test_distance_trace_rows_engines(pcs, oracle, monkeypatch, morton):
     np.testing.assert_array_equal(tr, wtr)
 
 
-def test_batched_configs_vs_oracle(oracle):
+def test_batched_configs_vs_oracle(oracle, npdu_engine):
     import torch
 
     from paper_2208_08795_b200 import sample
@@ -167,7 +176,7 @@ def test_batched_configs_vs_oracle(oracle):
         np.testing.assert_array_equal(res[1].cpu().numpy(), want_st.astype(np.int64), err_msg=name)
 
 
-def test_random_first_and_per_cloud_seeds(oracle):
+def test_random_first_and_per_cloud_seeds(oracle, npdu_engine):
     import torch
 
     from paper_2208_08795_b200 import sample
@@ -431,7 +440,7 @@ def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
 
 
 @pytest.mark.parametrize("index_dtype", ["int32", "int64"])
-def test_npdu_tmem_slow_path_and_output_blocks(oracle, index_dtype):
+def test_npdu_tmem_slow_path_and_output_blocks(oracle, npdu_engine, index_dtype):
     """fp32 NPDU sectors <= 4096 points (the TMEM kernel, 1-4 rows per lane): heavily duplicated
     clouds drive the all-zero slow path (lowest unsampled index) many times;
     quotas that are not multiples of 32 exercise the buffered output flush."""
@@ -509,7 +518,7 @@ def _core_sample(meth, pts, c, m, k):
     ("fps", 3, 1, 1, 1, 0), ("afps", 2, 5, 5, 5, 0), ("npdu_afps", 2, 7, 7, 7, 1),
     ("npdu_fps", 2, 40, 40, 1, 1), ("npdu_fps", 2, 40, 17, 1, 1000), ("afps", 5000, 2, 2, 1, 0),
     ("npdu_afps", 300, 96, 33, 3, 3), ("fps", 2, 4096, 1, 1, 0), ("afps", 1, 3073, 3073, 1, 0)])
-def test_edge_shapes(oracle, meth, B, n, c, m, k):
+def test_edge_shapes(oracle, npdu_engine, meth, B, n, c, m, k):
     """Degenerate shapes: one point, quota 1, every point sampled, window 1,
     window wider than the sector, thousands of two-point clouds."""
     import torch
@@ -633,6 +642,24 @@ def test_host_pipelined_path_matches_device_path():
                  first="random", seed=3, index_dtype=torch.int64)
     np.testing.assert_array_equal(h64[0], d64[0].cpu().numpy())
     np.testing.assert_array_equal(h64[1], d64[1].cpu().numpy())
+
+
+def test_host_batch_chunk_schedules():
+    """pcs_sample_host_batch chunk boundaries: the default schedule, uneven
+    chunks, more chunks than the stream events hold, and one chunk per cloud
+    all give the device path's results."""
+    import torch
+
+    from paper_2208_08795_b200 import sample, sample_host_batch
+
+    xyz = synth.lidar_sweep(2, seed=7)[:, :4096].copy()
+    xyz = np.concatenate([xyz] * 19 + [xyz[:1]])  # 39 clouds
+    dev = sample(torch.from_numpy(xyz).cuda(), 1024, method="npdu_afps", m=4, k=129)
+    pinned = torch.from_numpy(xyz).pin_memory()
+    for chunks in (0, 5, 39, 100):
+        h = sample_host_batch(pinned, 1024, method="npdu_afps", m=4, k=129, chunks=chunks)
+        np.testing.assert_array_equal(h[0], dev[0].cpu().numpy(), err_msg=str(chunks))
+        np.testing.assert_array_equal(h[1], dev[1].cpu().numpy(), err_msg=str(chunks))
 
 
 def test_one_million_point_afps_vs_oracle(oracle):
