@@ -58,6 +58,21 @@ __device__ __forceinline__ void row_key(double dj, int r, uint32_t& hi, uint32_t
   j = static_cast<uint32_t>((r << 5) + __ffs(cand) - 1);
 }
 
+// Row key with the index deferred: (max d, ballot of the lanes holding it).
+// Rows order their indices (row r < row r' => every index smaller), so the
+// sector argmax only needs the lowest row among equal maxima, and the lane
+// within it (ffs of the ballot) is resolved once, for the winning row.
+__device__ __forceinline__ void row_key_mask(double dj, uint32_t& hi, uint32_t& lo,
+                                             uint32_t& mask) {
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(dj));
+  const uint32_t h = static_cast<uint32_t>(bits >> 32), l = static_cast<uint32_t>(bits);
+  const uint32_t mh = __reduce_max_sync(kFull, h);
+  const uint32_t ml = __reduce_max_sync(kFull, h == mh ? l : 0u);
+  mask = __ballot_sync(kFull, h == mh && l == ml);
+  hi = mh;
+  lo = ml;
+}
+
 template <bool F2F>
 __device__ __forceinline__ double to_f64(float v) { return F2F ? static_cast<double>(v) : widen_f32(v); }
 template <bool F2F>
@@ -431,13 +446,15 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     if (p.out_sector)
       for (int i = lane; i < g.quota; i += 32)
         p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
-    uint32_t rm_hi[RPL], rm_lo[RPL], rm_j[RPL];
+    // cached row keys (row r = lane + 32 i): max d and the ballot of lanes
+    // holding it (index deferred, row_key_mask)
+    uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL];
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = lane + 32 * i;
       rm_hi[i] = r < rows ? kInfHi : 0u;
       rm_lo[i] = 0u;
-      rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
+      rm_m[i] = r < rows ? 1u : 0u;
     }
     GroupSetup gs;
     gs.b = b;
@@ -497,17 +514,28 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
-        uint32_t hi, lo, jj;
-        row_key(dj[q], r_lo + q, hi, lo, jj);
-        store_row<RPL>(r_lo + q, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+        uint32_t hi, lo, mk;
+        row_key_mask(dj[q], hi, lo, mk);
+        store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
       }
-      uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
+      // this lane's best row (rows grow with i: strict > keeps the lowest),
+      // then the warp's: max d, lowest row among equals, its lowest lane
+      uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
 #pragma unroll
       for (int i = 1; i < RPL; ++i)
-        if (rows::key_gt(rm_hi[i], rm_lo[i], rm_j[i], hi, lo, j)) {
-          hi = rm_hi[i]; lo = rm_lo[i]; j = rm_j[i];
+        if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
+          hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
         }
-      warp_argmax(hi, lo, j);
+      uint32_t j;
+      {
+        const uint32_t mh = __reduce_max_sync(kFull, hi);
+        const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+        const uint32_t mr = __reduce_min_sync(kFull, (hi == mh && lo == ml) ? rsel : kNoIndex);
+        const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
+        hi = mh;
+        lo = ml;
+        j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+      }
       if ((hi | lo) == 0u) {
         // fold outputs [marked, it) into the bitmap: whole blocks from
         // global memory, the current block from the lanes' buffers
