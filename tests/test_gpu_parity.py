@@ -463,6 +463,30 @@ def test_npdu_tmem_slow_path_and_output_blocks(oracle, npdu_engine, index_dtype)
             np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("grid", [0, 8, 64, 1 << 20])
+def test_npdu_tmem_high_word_ties(oracle, monkeypatch, grid):
+    """TMEM NPDU kernel row keys under ties: coordinates on a coarse grid
+    (many equal distances), a fine grid (high words of d tie, low words
+    differ) and uniform ones, every sector size family."""
+    import torch
+
+    from paper_2208_08795_b200 import sample
+
+    monkeypatch.setenv("PCS_NPDU_WIDE", "0")
+    rng = np.random.default_rng(grid + 1)
+    for n, c, m, k in ((1024, 256, 1, 129), (4096, 1024, 4, 65), (2048, 700, 1, 33),
+                       (3000, 900, 2, 97), (512, 200, 1, 65), (8192, 2048, 8, 129)):
+        xyz = synth.uniform_cube(4, n, n + grid)
+        if grid:
+            xyz = (np.round(xyz * grid) / grid).astype(np.float32)
+        if grid == 1 << 20:  # distances within a few ulps of each other
+            xyz = (1.0 + rng.integers(0, 4, xyz.shape) * 2.0 ** -22).astype(np.float32)
+        idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="npdu_afps", m=m, k=k)
+        want_idx, want_st = oracle.sample_batch_f32("npdu_afps", xyz, c, m, k)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{n} {grid}")
+        np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_streaming_engine_beyond_on_chip_sectors(oracle):
     """Sectors larger than every on-chip engine (d[] in global memory, one
     cooperative launch per sector, grid barrier per iteration): FPS and NPDU
