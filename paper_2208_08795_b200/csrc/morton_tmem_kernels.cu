@@ -568,12 +568,22 @@ cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
 
 }  // namespace
 
-// Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory).
+// Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory),
+// at least cs_min CTAs for batches of few sectors.
+constexpr int kMortonSpreadMax = 1;
 cudaError_t run_morton_tmem_any(SampleParams p, long long n, cudaStream_t st) {
   // fp32 batches; distance traces come from the fp64 drop-in (other engines)
   if (p.f64 || p.trace) return cudaErrorNotSupported;
   const long long srows = (n + 31) / 32;
-  for (int CS = 1; CS <= 16; CS *= 2) {
+  // Few sectors: spread each over more SMs (a larger cluster) while the
+  // batch still fits one CTA per SM -- the per-iteration row work shrinks
+  // with the CTA's share. PCS_MORTON_CS_MIN overrides (A/B).
+  int cs_min = 1;
+  const long long sectors = p.B * p.M;
+  while (cs_min < kMortonSpreadMax && sectors * cs_min * 2 <= 148 && srows >= 64LL * cs_min * 2)
+    cs_min *= 2;
+  if (const char* e = std::getenv("PCS_MORTON_CS_MIN")) cs_min = std::max(1, std::atoi(e));
+  for (int CS = cs_min; CS <= 16; CS *= 2) {
     const int rows = static_cast<int>((srows + CS - 1) / CS);
     if (rows > 512) continue;
     const int W = morton_tmem_w(rows, p.B * p.M);
