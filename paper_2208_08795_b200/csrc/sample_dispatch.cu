@@ -46,7 +46,9 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   // TMEM row engine in storage order, rows restricted to the window
   // (PCS_NPDU_BIG=0 keeps the warp / shared-memory row kernels)
   const char* nb = std::getenv("PCS_NPDU_BIG");
-  if (e == cudaErrorNotSupported && !rows && windowed && !p.f64 && nmax_sector > 4096 &&
+  const char* nbm = std::getenv("PCS_NPDU_BIG_MIN");  // A/B: crossover (points per sector)
+  const long long big_min = nbm ? std::atoll(nbm) : 4096;
+  if (e == cudaErrorNotSupported && !rows && windowed && !p.f64 && nmax_sector > big_min &&
       !(nb && std::string(nb) == "0"))
     e = run_morton_tmem_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && !rows)
