@@ -11,7 +11,10 @@ from paper_2208_08795_b200 import synth  # noqa: E402
 x = torch.from_numpy(synth.uniform_cube(3, 4099, 1)).cuda()
 pcs.sample(x, 300, method="fps")                              # Morton TMEM
 pcs.sample(x, 300, method="afps", m=4)                        # full kernel
-pcs.sample(x, 300, method="npdu_afps", m=4, k=129)            # NPDU TMEM
+pcs.sample(x, 300, method="npdu_afps", m=4, k=129)            # NPDU wide (<= 148 sectors)
+xb = torch.from_numpy(synth.uniform_cube(40, 4099, 4)).cuda()
+pcs.sample(xb, 300, method="npdu_afps", m=4, k=129)           # NPDU TMEM (160 sectors)
+pcs.sample(xb[:, :1000], 300, method="npdu_afps", m=1, k=65)  # NPDU wide, P=4
 pcs.sample(x, 300, method="npdu_fps", k=65)                   # TMEM rows, window mode
 pcs.sample(x.double(), 300, method="fps")                     # Morton smem (fp64)
 pcs.sample(x.double(), 300, method="npdu_afps", m=2, k=33)    # NPDU warp kernel
@@ -30,6 +33,7 @@ del os.environ["PCS_SAMPLER"], os.environ["PCS_MORTON"]
 pts = synth.random_cloud(500, 3)
 pcs.fps(pts, 50)
 pcs.npdu_afps(pts, 50, 5, 9)
+pcs.local_fps(pts, 10, 400, 30, k=7, trace=True)              # wide kernel, fp64 + trace
 pcs.sample_host_batch(synth.uniform_cube(4, 1000, 3), 100, method="npdu_afps", m=2, k=33, sort="x")
 idx = pcs.sample(x, 100, method="afps", m=2)[0]
 pcs.quality(x, idx)
