@@ -192,9 +192,10 @@ def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
                   env: Optional[str] = None, dtype: str = "float32", batch: int = 1) -> str:
     """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
     the per-sector register kernel for full windows up to 3072 points, the
-    Morton-row engine for larger full windows (one CTA or a cluster), the
-    TMEM / warp NPDU kernels for windows over sectors up to 8192 points, the
-    storage-order row engine otherwise."""
+    Morton-row engine for larger full windows (one CTA or a cluster), for
+    windows over sectors up to 4096 points the 8-warp latency form when the
+    call has at most 148 sectors, else the TMEM / warp NPDU kernels (up to
+    8192 points), the storage-order row engine otherwise."""
     import os
 
     sectored = method in ("afps", "npdu_afps")
