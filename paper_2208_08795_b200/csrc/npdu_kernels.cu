@@ -44,20 +44,6 @@ __host__ __device__ __forceinline__ size_t npdu_warp_bytes(int nmax, int rmax) {
   return (np * (8 + (GC ? 0 : 3 * sizeof(CT))) + np / 8 + 15) & ~size_t(15);
 }
 
-// (max d, min index) of row r. Within a row the index grows with the lane,
-// so the lowest lane holding the max is the winner.
-__device__ __forceinline__ void row_key(double dj, int r, uint32_t& hi, uint32_t& lo,
-                                        uint32_t& j) {
-  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(dj));
-  const uint32_t h = static_cast<uint32_t>(bits >> 32), l = static_cast<uint32_t>(bits);
-  const uint32_t mh = __reduce_max_sync(kFull, h);
-  const uint32_t ml = __reduce_max_sync(kFull, h == mh ? l : 0u);
-  const unsigned cand = __ballot_sync(kFull, h == mh && l == ml);
-  hi = mh;
-  lo = ml;
-  j = static_cast<uint32_t>((r << 5) + __ffs(cand) - 1);
-}
-
 // Row key with the index deferred: (max d, ballot of the lanes holding it).
 // Rows order their indices (row r < row r' => every index smaller), so the
 // sector argmax only needs the lowest row among equal maxima, and the lane
@@ -139,13 +125,14 @@ __global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
       p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
   // row maxima: lane l caches row r = l + 32*i in slot i; initially every
   // point is +inf, so a row's winner is its first point
-  uint32_t rm_hi[RPL], rm_lo[RPL], rm_j[RPL];
+  // (key = max d and the ballot of the lanes holding it, row_key_mask)
+  uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL];
 #pragma unroll
   for (int i = 0; i < RPL; ++i) {
     const int r = lane + 32 * i;
     rm_hi[i] = r < rows ? kInfHi : 0u;
     rm_lo[i] = 0u;
-    rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
+    rm_m[i] = r < rows ? 1u : 0u;
   }
   GroupSetup gs;
   gs.b = b;
@@ -199,9 +186,9 @@ __global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
         if (lower[q]) d[j0 + 32 * q] = dist[q];
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
-        uint32_t hi, lo, jj;
-        row_key(dj[q], r_lo + q, hi, lo, jj);
-        store_row<RPL>(r_lo + q, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+        uint32_t hi, lo, mk;
+        row_key_mask(dj[q], hi, lo, mk);
+        store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
       }
     } else {
       const int r_hi = (we - 1) >> 5;
@@ -217,11 +204,11 @@ __global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
         if (lb) d[jb] = eb;
         da = la ? ea : da;
         db = lb ? eb : db;
-        uint32_t hi, lo, jj;
-        row_key(da, r, hi, lo, jj);
-        store_row<RPL>(r, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
-        row_key(db, r + 1, hi, lo, jj);
-        store_row<RPL>(r + 1, lane, hi, lo, jj, rm_hi, rm_lo, rm_j);
+        uint32_t hi, lo, mk;
+        row_key_mask(da, hi, lo, mk);
+        store_row<RPL>(r, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
+        row_key_mask(db, hi, lo, mk);
+        store_row<RPL>(r + 1, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
       }
     }
     if (trace) {
@@ -230,15 +217,26 @@ __global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
     }
     // whole-sector argmax from the cached row maxima; rows l + 32*i grow with
     // i, so a strict > keeps the lowest index among equal distances
-    uint32_t hi = rm_hi[0], lo = rm_lo[0], j = rm_j[0];
+    uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
 #pragma unroll
     for (int i = 1; i < RPL; ++i) {
       const bool gt = rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo);
       hi = gt ? rm_hi[i] : hi;
       lo = gt ? rm_lo[i] : lo;
-      j = gt ? rm_j[i] : j;
+      mk = gt ? rm_m[i] : mk;
+      rsel = gt ? static_cast<uint32_t>(lane + 32 * i) : rsel;
     }
-    warp_argmax(hi, lo, j);
+    // max d, lowest row among equals, its lowest lane (rows order indices)
+    uint32_t j;
+    {
+      const uint32_t mh = __reduce_max_sync(kFull, hi);
+      const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+      const uint32_t mr = __reduce_min_sync(kFull, (hi == mh && lo == ml) ? rsel : kNoIndex);
+      const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
+      hi = mh;
+      lo = ml;
+      j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+    }
     if ((hi | lo) == 0u) {
       // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
       uint32_t jm = kNoIndex;
