@@ -444,15 +444,20 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     if (p.out_sector)
       for (int i = lane; i < g.quota; i += 32)
         p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
-    // cached row keys (row r = lane + 32 i): max d and the ballot of lanes
-    // holding it (index deferred, row_key_mask)
+    // cached row keys (row r = lane + 32 i): max d and either the ballot of
+    // the lanes holding it (index deferred to the winning row, kBallot) or
+    // the index itself. The ballot form saves instructions per row and wins
+    // with 5-row windows (cfg4 0.385 -> 0.357 ms); with 3-row windows the
+    // index form measured faster (cfg3 / cfg5 NPDU 8K kernels 0.059 / 0.116
+    // vs 0.065 / 0.123 ms).
+    constexpr bool kBallot = RMAX >= 5;
     uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL];
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = lane + 32 * i;
       rm_hi[i] = r < rows ? kInfHi : 0u;
       rm_lo[i] = 0u;
-      rm_m[i] = r < rows ? 1u : 0u;
+      rm_m[i] = kBallot ? (r < rows ? 1u : 0u) : (r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex);
     }
     GroupSetup gs;
     gs.b = b;
@@ -514,6 +519,7 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       for (int q = 0; q < RMAX; ++q) {
         uint32_t hi, lo, mk;
         row_key_mask(dj[q], hi, lo, mk);
+        if constexpr (!kBallot) mk = static_cast<uint32_t>(((r_lo + q) << 5) + __ffs(mk) - 1);
         store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
       }
       // this lane's best row (rows grow with i: strict > keeps the lowest),
@@ -524,8 +530,10 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
         if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
           hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
         }
-      uint32_t j;
-      {
+      uint32_t j = mk;
+      if constexpr (!kBallot) {
+        warp_argmax(hi, lo, j);
+      } else {
         const uint32_t mh = __reduce_max_sync(kFull, hi);
         const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
         const uint32_t mr = __reduce_min_sync(kFull, (hi == mh && lo == ml) ? rsel : kNoIndex);
