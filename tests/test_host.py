@@ -200,3 +200,21 @@ def test_cli_usage_errors_exit_2():
 
     assert cli.main(["sample"]) == 2
     assert cli.main(["frobnicate"]) == 2
+
+
+def test_kernel_family_mirrors_dispatch(pcs, monkeypatch):
+    """ops.kernel_family follows csrc/sample_dispatch.cu + run_npdu_any: the
+    8-warp NPDU form for calls of <= 148 sectors (PCS_NPDU_WIDE moves it),
+    the one-warp TMEM kernel above, full / Morton kernels for full windows."""
+    for var in ("PCS_NPDU_WIDE", "PCS_SAMPLER", "PCS_MORTON", "PCS_MORTON_MIN", "PCS_NPDU_TMEM"):
+        monkeypatch.delenv(var, raising=False)
+    kf = pcs.kernel_family
+    assert kf("npdu_afps", 32768, 32, 129, batch=4) == "npdu_wide_kernel"      # 128 sectors
+    assert kf("npdu_afps", 32768, 32, 129, batch=5) == "npdu_tmem_kernel"      # 160 sectors
+    assert kf("npdu_afps", 32768, 32, 129, batch=128) == "npdu_tmem_kernel"    # cfg4
+    assert kf("npdu_fps", 4096, 1, 65, batch=1) == "npdu_wide_kernel"
+    assert kf("npdu_fps", 8192, 1, 65, batch=1) == "morton_tmem_kernel"        # > 4096 points
+    assert kf("afps", 2048, 8, batch=16) == "fps_full_kernel"                  # cfg2
+    assert kf("fps", 8192, 1, batch=64) == "morton_tmem_kernel"                # cfg3 FPS
+    monkeypatch.setenv("PCS_NPDU_WIDE", "0")
+    assert kf("npdu_afps", 32768, 32, 129, batch=1) == "npdu_tmem_kernel"
