@@ -220,13 +220,17 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
   const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
-  // Chunk boundaries: `chunks` (<= 0: 8) equal chunks. (Splitting the last
+  // Chunk boundaries: `chunks` equal chunks (<= 0: by input size). (Splitting the last
   // chunk s/2, s/4, s/4 so its sectors take the lower-latency W-warp NPDU
   // kernel measured slower: cfg4 e2e 1.14 -> 1.22 ms, the small chunks'
   // kernels overlap on the worker streams.)
   std::vector<int64_t> bounds{0};
   {
-    const int64_t nu = std::min<int64_t>(std::min<int64_t>(B, chunks > 0 ? chunks : 8), kEvents - 4);
+    // default: one chunk per ~4 MiB of input, at most 8 (small batches are
+    // dominated by per-chunk API and launch overhead, not by the copy)
+    const int64_t by_size = static_cast<int64_t>((cloud_bytes * B) >> 22);
+    const int64_t def = std::max<int64_t>(1, std::min<int64_t>(8, by_size));
+    const int64_t nu = std::min<int64_t>(std::min<int64_t>(B, chunks > 0 ? chunks : def), kEvents - 4);
     for (int64_t i = 1; i <= nu; ++i) bounds.push_back(B * i / nu);
   }
   int nch = static_cast<int>(bounds.size()) - 1;
