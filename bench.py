@@ -7,21 +7,34 @@
 Metric (BASELINE.json): sampled points/s (and clouds/s), whole job. A step is
 one pass of the hot path over one batch resident in HBM: the per-cloud stable
 axis sort (when the config sorts) plus the sampler, both hand-written sm_100a
-kernels. Weak scaling: every rank samples its own batch of the configured
-size (clouds are independent, no collective on the data path). Timing: CUDA
-events on the launching stream around each step, an L2 flush (a 512 MiB
-write, > 126 MB L2) between steps outside the events, barrier + synchronize on
-both sides of the K timed steps, max over ranks.
+kernels. Timing: CUDA events on the launching stream around each step, an L2
+flush (a 512 MiB write, > 126 MB L2) between steps outside the events,
+barrier + synchronize on both sides of the K timed steps, max over ranks.
 
-Also reported: `e2e` (the same metric through the public API with host
-buffers: pinned H2D of the batch, sort + sample, D2H of indices + stats, every
-step), `roofline` (the sampler kernel's FP64 work against the measured FP64
-peak), `cpu_baseline` (the unmodified reference, oracle/_ref, on this host's
-cores, bounded sample), `clocks` (nvidia-smi during the timed region).
+Multi-GPU (BASELINE cfg4 "batch 128 sharded across 8 GPUs"): the batch is
+split by cloud, rank r sampling clouds shard.split(B, N, r) -- strong
+scaling, the job's work is fixed; a single large cloud (cfg5-1m) splits by
+sector run. The weak-scaling form (every rank its own full batch) is
+reported beside it as `weak`.
+
+Also reported: `e2e` (the same metric through the public C-ABI host entry
+with host buffers -- pinned H2D of the batch, sort + sample, D2H of indices
++ stats -- timed with the host clock around the synchronous call),
+`roofline` (the sampler kernel's FP64 work against the measured FP64 peak),
+`cpu_baseline` (the unmodified reference, oracle/_ref, on this host's cores,
+bounded sample, best of 3), `parity` (the timed output against the
+reference's indices for the cpu_baseline's clouds), `workloads` (every
+BASELINE config measured the same way, N=1 only), `clocks` (nvidia-smi
+during the timed region).
+
+The reference arm never loads the CUDA library: the generators are loaded
+by file path (paper_2208_08795_b200/synth.py is plain numpy), not through
+the package, whose import loads libpcs_gpu.so.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import subprocess
@@ -46,7 +59,7 @@ WORKLOADS = {
 for _n in (2048, 4096, 8192, 16384, 32768):
     WORKLOADS[f"cfg5-fps-{_n}"] = dict(gen="cube", B=256, N=_n, method="fps", C=_n // 4, M=1,
                                        K=None, sort="x")
-    for _m in (4, 16, 64, 256):
+    for _m in (1, 4, 16, 64, 256):
         WORKLOADS[f"cfg5-afps{_m}-{_n}"] = dict(gen="cube", B=256, N=_n, method="afps",
                                                 C=_n // 4, M=_m, K=None, sort="x")
     WORKLOADS[f"cfg5-npdu-{_n}"] = dict(gen="cube", B=256, N=_n, method="npdu_afps", C=_n // 4,
@@ -55,7 +68,11 @@ for _n in (2048, 4096, 8192, 16384, 32768):
 # one 1M-point cloud: under torchrun its sectors are split across the ranks
 # (strong scaling, BASELINE cfg5), each rank sorting the cloud itself
 WORKLOADS["cfg5-1m"] = dict(gen="cube", B=1, N=1 << 20, method="afps", C=(1 << 20) // 4, M=1024,
-                            K=None, sort="x", strong=True)
+                            K=None, sort="x")
+# the streaming vanilla-FPS engine (north_star item 4): one cloud too large
+# for any on-chip engine, d[] in global memory
+WORKLOADS["stream-fps-1m"] = dict(gen="cube", B=1, N=1 << 20, method="fps", C=2048, M=1,
+                                  K=None, sort="x")
 
 # latency probes: one NPDU sector per warp, 1 warp / 148 warps / 4096 warps
 for _b in (1, 148, 4096):
@@ -63,12 +80,31 @@ for _b in (1, 148, 4096):
                                        K=129, sort=None)
 
 DEFAULT_WORKLOAD = "cfg4"
+# the `workloads` object of the default run: every BASELINE config
+SWEEP = (["cfg1", "cfg2", "cfg3", "cfg3-afps", "cfg3-fps", "cfg4"]
+         + [f"cfg5-{v}-{n}" for n in (2048, 4096, 8192, 16384, 32768)
+            for v in ("fps", "afps1", "afps4", "afps16", "afps64", "afps256", "npdu")]
+         + ["cfg5-1m", "stream-fps-1m"])
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+HBM_FALLBACK_GBS = 6543.7  # MEASURED_PEAKS.json of this pool (r01/r02)
+
+
+def _synth():
+    """paper_2208_08795_b200/synth.py loaded by path: plain numpy, and the
+    package import (which loads the CUDA library) stays out of the
+    reference arm."""
+    mod = sys.modules.get("pcs_synth_bench")
+    if mod is None:
+        path = os.path.join(ROOT, "paper_2208_08795_b200", "synth.py")
+        spec = importlib.util.spec_from_file_location("pcs_synth_bench", path)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        sys.modules["pcs_synth_bench"] = mod
+    return mod
 
 
 def make_input(w, seed_base=0):
-    from paper_2208_08795_b200 import synth
-
+    synth = _synth()
     g = w["gen"]
     if g == "cube":
         return synth.uniform_cube(w["B"], w["N"], seed_base)
@@ -77,6 +113,12 @@ def make_input(w, seed_base=0):
     if g == "lidar":
         return synth.lidar_sweep(w["B"], seed=seed_base + 4)
     raise ValueError(g)
+
+
+def host_sorted(w, xyz):
+    if w["sort"] is None:
+        return xyz
+    return _synth().stable_sort_np(xyz, "xyz".index(w["sort"]))[0]
 
 
 class ClockSampler:
@@ -129,54 +171,37 @@ class ClockSampler:
                 "samples": len(loaded)}
 
 
+def _json_file(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def ncu_traffic(workload):
     """DRAM bytes per launch of the sampler kernel (and its issue rate) from
-    the committed ncu --set full summary for this workload
-    (profiles/ncu_traffic.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)[workload]
-        return float(d["dram_bytes"]), d["source"], d.get("ipc_per_sm")
-    except (OSError, KeyError, ValueError):
-        return None, "no ncu capture for this workload", None
+    the committed ncu --set full capture for this workload
+    (profiles/ncu_traffic.json, made by tools/ncu_sweep.sh)."""
+    d = _json_file("ncu_traffic.json").get(workload)
+    if not d:
+        return None, "no ncu capture for this workload", None, None
+    return float(d["dram_bytes"]), d["source"], d.get("ipc_per_sm"), d.get("fp64_pipe_pct")
 
 
 def fp64_peak():
-    try:
-        with open(FP64_PEAK_FILE) as f:
-            d = json.load(f)
+    d = _json_file("fp64_peak.json")
+    if "fp64_tflops" in d:
         return float(d["fp64_tflops"]), d.get("source", FP64_PEAK_FILE)
+    return None, "missing"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except (OSError, KeyError, ValueError):
-        return None, "missing"
-
-
-def cpu_reference(w, xyz_sorted, budget_s=20.0, steps=1, quiet=False):
-    """The unmodified reference (oracle/_ref) on the host: one cloud per
-    worker thread, sampler at threads=1 (proj/src/bench.cpp:90-92,104-120),
-    timed around the sampler calls only, best of `steps` runs. Bounded: a
-    prefix of the batch sized to ~budget_s of single-core work."""
-    from oracle import Reference
-
-    ref = Reference()
-    workers = os.cpu_count() or 1
-    probe = xyz_sorted[:1]
-    _, _, t1 = ref.sample_batch_f32(w["method"], probe, w["C"], w["M"], w["K"] or 0, workers=1)
-    per_cloud = max(t1, 1e-6)
-    nb = int(max(1, min(w["B"], budget_s / per_cloud)))
-    nb = max(min(nb, w["B"]), min(w["B"], workers))
-    sample = xyz_sorted[:nb]
-    best = None
-    for _ in range(max(1, steps)):
-        _, _, secs = ref.sample_batch_f32(w["method"], sample, w["C"], w["M"], w["K"] or 0,
-                                          workers=workers)
-        best = secs if best is None else min(best, secs)
-    pts_s = nb * w["C"] / best
-    return {"value": pts_s, "unit": "sampled points/s", "cores": min(workers, nb),
-            "kind": "reference", "clouds_per_s": nb / best,
-            "sample": f"{nb} of {w['B']} clouds of the same batch (pre-sorted on the host), "
-                      f"{min(workers, nb)} worker threads, best of {max(1, steps)}, "
-                      f"single-core probe {per_cloud * 1e3:.2f} ms/cloud",
-            "cpu_model": _cpu_model()}
+        return HBM_FALLBACK_GBS, "MEASURED_PEAKS.json absent: this pool's r01 measurement"
 
 
 def _cpu_model():
@@ -189,7 +214,80 @@ def _cpu_model():
     return "unknown"
 
 
-def launches_per_step(w):
+def cpu_reference(w, xyz_sorted, budget_s=20.0, repeats=3):
+    """The unmodified reference (oracle/_ref) on the host: one cloud per
+    worker thread, sampler at threads=1 (proj/src/bench.cpp:90-92,104-120),
+    timed around the sampler calls only, best of `repeats` runs
+    (proj/tests/acceptance_main.cpp:63-71). Bounded: a prefix of the batch
+    sized to ~budget_s of single-core work; a single cloud runs the
+    reference's own sector threading (threads = cores, sampler.cpp:25-46)
+    and, when even that is too long, its first c' picks (FPS is greedy: the
+    first c' picks of a run equal a run with c = c').
+
+    Returns the baseline dict plus the reference's indices for the sampled
+    clouds (the parity check)."""
+    from oracle import Reference
+
+    ref = Reference()
+    workers = os.cpu_count() or 1
+    B, C = w["B"], w["C"]
+    if B == 1:
+        pts = xyz_sorted[0].astype(np.float64)
+        c = C
+        sectored = w["method"] in ("afps", "npdu_afps")
+        per_pick = None
+        if not sectored:
+            # time 64 picks single-threaded, then size the prefix
+            t0 = time.perf_counter()
+            ref.sample(w["method"], pts, min(64, C), 1, w["K"] or 0)
+            per_pick = (time.perf_counter() - t0) / min(64, C)
+            c = int(max(64, min(C, budget_s / max(per_pick, 1e-9))))
+        best, idx = None, None
+        for _ in range(max(1, repeats)):
+            t0 = time.perf_counter()
+            idx, _, _ = ref.sample(w["method"], pts, c, w["M"], w["K"] or 0,
+                                   threads=workers if sectored else 1)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res = {"value": c / best, "unit": "sampled points/s",
+               "cores": workers if sectored else 1, "kind": "reference",
+               "clouds_per_s": (c / C) / best,
+               "sample": (f"the 1 cloud, reference sector threads = {workers}, best of "
+                          f"{max(1, repeats)}" if sectored else
+                          f"the 1 cloud's first {c} of {C} picks (greedy prefix), 1 thread, "
+                          f"best of {max(1, repeats)}"),
+               "cpu_model": _cpu_model()}
+        return res, np.asarray(idx)[None, :], np.array([0])
+    probe = xyz_sorted[:1]
+    _, _, t1 = ref.sample_batch_f32(w["method"], probe, C, w["M"], w["K"] or 0, workers=1)
+    per_cloud = max(t1, 1e-6)
+    nb = int(max(1, min(B, budget_s / per_cloud)))
+    nb = max(min(nb, B), min(B, workers))
+    sample = xyz_sorted[:nb]
+    best, idx = None, None
+    for _ in range(max(1, repeats)):
+        idx, _, secs = ref.sample_batch_f32(w["method"], sample, C, w["M"], w["K"] or 0,
+                                            workers=workers)
+        best = secs if best is None else min(best, secs)
+    res = {"value": nb * C / best, "unit": "sampled points/s", "cores": min(workers, nb),
+           "kind": "reference", "clouds_per_s": nb / best,
+           "sample": f"{nb} of {B} clouds of the same batch (pre-sorted on the host), "
+                     f"{min(workers, nb)} worker threads, best of {max(1, repeats)}, "
+                     f"single-core probe {per_cloud * 1e3:.2f} ms/cloud",
+           "cpu_model": _cpu_model()}
+    return res, idx, np.arange(nb)
+
+
+def parity_of(gpu_idx, ref_idx, clouds):
+    """Mismatching clouds between the device output and the reference's
+    indices (a prefix of each row when the reference ran fewer picks)."""
+    c = ref_idx.shape[1]
+    bad = [int(b) for i, b in enumerate(clouds) if not np.array_equal(gpu_idx[b, :c], ref_idx[i])]
+    return {"clouds": int(len(clouds)), "picks_per_cloud": int(c), "mismatches": len(bad),
+            "mismatched_clouds": bad[:8], "against": "oracle/_ref (the unmodified reference)"}
+
+
+def launches_per_step(w, n_sort_launches=None):
     """Our kernels per step (csrc/sort_kernels.cu, csrc/sample_dispatch.cu):
     one sampler launch; the axis sort is one launch up to 256K fp32 points,
     otherwise the device-wide radix (histogram, scan, scatter per 8-bit
@@ -200,21 +298,26 @@ def launches_per_step(w):
     return 1 + sort
 
 
-def host_sorted(w, xyz):
-    if w["sort"] is None:
-        return xyz
-    from paper_2208_08795_b200 import synth
-
-    return synth.stable_sort_np(xyz, "xyz".index(w["sort"]))[0]
-
-
-def arm_config(workload, w, world, strong):
+def arm_config(workload, w, world, mode):
     """The `config` object both arms print (identical for the same workload)."""
-    return {"workload": workload, "clouds_per_gpu": w["B"], "points_per_cloud": w["N"],
+    return {"workload": workload, "clouds": w["B"], "points_per_cloud": w["N"],
             "samples_per_cloud": w["C"], "method": w["method"], "m": w["M"], "k": w["K"],
             "sort": w["sort"], "generator": w["gen"], "coords": "fp32 in, fp64 math",
             "l2": "flushed between steps (512 MiB write)",
-            "parallelism": (f"sector-split x{world}" if strong else f"dp{world}")}
+            "parallelism": {"batch": f"clouds split over {world} GPU(s)",
+                            "sector": f"sector-split x{world}",
+                            "weak": f"dp{world}"}[mode]}
+
+
+def _loaded_native():
+    """Shared objects of this repo mapped into the process (the reference
+    arm must show only oracle/ ones)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT))
 
 
 def run_reference_arm(args, w):
@@ -222,19 +325,213 @@ def run_reference_arm(args, w):
     if rank != 0:
         return 0
     xyz = make_input(w)
-    res = cpu_reference(w, host_sorted(w, xyz), budget_s=8.0, steps=args.steps)
+    res, _, _ = cpu_reference(w, host_sorted(w, xyz), budget_s=8.0, repeats=args.steps)
+    mode = "sector" if (w["B"] == 1 and args.gpus > 1) else "batch"
     line = {"metric": "sampled points/s", "value": res["value"], "unit": "sampled points/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": arm_config(args.workload, w, args.gpus,
-                                 bool(w.get("strong")) and args.gpus > 1),
+            "config": arm_config(args.workload, w, args.gpus, mode),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "clouds_per_s": res["clouds_per_s"], "cpu_model": res["cpu_model"],
             "e2e": {"value": res["value"], "unit": "sampled points/s",
-                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_libraries": _loaded_native()}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------- GPU arm
+class Runner:
+    """One workload on this rank's GPU: the step (sort + sample), the sort
+    and the sampler alone, the host-buffer e2e call."""
+
+    def __init__(self, pcs, torch, dev, w, xyz_host, shard_spec=None):
+        self.pcs, self.torch, self.dev, self.w = pcs, torch, dev, w
+        self.xyz_host = xyz_host
+        self.xyz = torch.from_numpy(xyz_host).to(dev)
+        self.sh = shard_spec  # sector shard of one large cloud, or None
+        self.flush = None
+
+    def sample_sorted(self, xs):
+        w, pcs, sh = self.w, self.pcs, self.sh
+        if sh is None:
+            return pcs.sample(xs, w["C"], method=w["method"], m=w["M"], k=w["K"])
+        return pcs.sample(xs[:, sh.point_lo:sh.point_hi], sh.c, method=w["method"], m=sh.m,
+                          k=w["K"], index_base=sh.point_lo, sector_base=sh.sector_lo)
+
+    def step(self, x):
+        w, pcs = self.w, self.pcs
+        if self.sh is None:
+            return pcs.sample(x, w["C"], method=w["method"], m=w["M"], k=w["K"], sort=w["sort"])
+        xs = pcs.sort_axis(x, w["sort"])[0] if w["sort"] else x
+        return self.sample_sorted(xs)
+
+    def _flush(self, i):
+        if self.flush is None:
+            self.flush = self.torch.empty(512 * 1024 * 1024 // 4, dtype=self.torch.float32,
+                                          device=self.dev)
+        self.flush.fill_(float(i))
+
+    def timed(self, fn, steps, per_step_sync=False):
+        """Sum of CUDA-event times of `fn` over `steps` calls, L2 flushed
+        before each (outside the events). Returns (ms_total, last output)."""
+        torch = self.torch
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        out = None
+        for i in range(steps):
+            self._flush(i)
+            starts[i].record()
+            out = fn()
+            ends[i].record()
+            if per_step_sync:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        return sum(s.elapsed_time(e) for s, e in zip(starts, ends)), out
+
+    def e2e(self, steps, warmup, world=1, dist=None):
+        """The C-ABI host entry (pcs_sample_host_batch): pinned batch in,
+        host arrays out, one synchronous native call per step, timed with
+        the host clock after the flush has completed."""
+        torch, w, pcs = self.torch, self.w, self.pcs
+        pinned = torch.from_numpy(self.xyz_host).pin_memory()
+        sh = self.sh
+
+        def call():
+            if sh is None:
+                return pcs.sample_host_batch(pinned, w["C"], method=w["method"], m=w["M"],
+                                             k=w["K"], sort=w["sort"])
+            res = self.step(pinned.to(self.dev, non_blocking=True))
+            return tuple(t.cpu() for t in res)
+
+        # warm-up: at least W steps and 0.5 s -- the host link ramps up over
+        # the first ~15 transfers after idling (tools/e2e_dbg.py)
+        t_warm = time.perf_counter()
+        for i in range(max(warmup, 1000)):
+            call()
+            if i + 1 >= warmup and time.perf_counter() - t_warm > 0.5:
+                break
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        total = 0.0
+        r = None
+        for i in range(steps):
+            self._flush(i)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = call()
+            total += time.perf_counter() - t0
+        e_ms = total * 1e3
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e_ms /= steps
+        # the PCIe floor on this box: one plain H2D of the same pinned batch
+        dst = torch.empty(pinned.shape, dtype=pinned.dtype, device=self.dev)
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h2d = []
+        for _ in range(5):
+            es.record()
+            dst.copy_(pinned, non_blocking=True)
+            ee.record()
+            torch.cuda.synchronize()
+            h2d.append(es.elapsed_time(ee))
+        del dst
+        nbytes = pinned.numel() * pinned.element_size()
+        return {"ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
+                "h2d_gbps": nbytes / min(h2d) / 1e6, "h2d_bytes_per_step": int(nbytes),
+                "d2h_bytes_per_step": int(sum(t.nbytes if hasattr(t, "nbytes") else
+                                              t.numel() * t.element_size() for t in r)),
+                "timer": "host perf_counter around the synchronous call, after "
+                         "torch.cuda.synchronize() on the L2 flush",
+                "path": ("C-ABI pcs_sample_host_batch (pinned host tensor in, host arrays "
+                         "out): chunked H2D overlapped with sort+sample, D2H of indices, "
+                         "stats (and perm when sorting)") if sh is None else
+                        "pinned H2D, sort, sample of this rank's sectors, D2H"}
+
+
+def sort_bytes(w):
+    """Algorithmic HBM bytes of the axis sort per step: read the cloud (12N),
+    write the permutation (4N) and the gathered cloud (12N)."""
+    return 0 if not w["sort"] else w["B"] * w["N"] * 28
+
+
+def stream_bytes(w):
+    """the streaming engine's algorithmic bytes per cloud,
+    (C-1)*N*28 (xyz 12 B read, d 8 B read + 8 B written per point and
+    iteration) + 12N + 4C."""
+    return w["B"] * ((w["C"] - 1) * w["N"] * 28 + 12 * w["N"] + 4 * w["C"])
+
+
+def measure_workload(pcs, torch, dev, name, w, steps, warmup, xyz_host, cpu_budget_s=2.0):
+    """One `workloads` entry (N=1): step / sort / sampler times, kernel,
+    roofline fractions, e2e, cpu_baseline and parity."""
+    r = Runner(pcs, torch, dev, w, xyz_host)
+    for _ in range(warmup):
+        out = r.step(r.xyz)
+    torch.cuda.synchronize()
+    evals = int(out[1][:, 0].sum().item())
+    ms, out = r.timed(lambda: r.step(r.xyz), steps)
+    ms /= steps
+    gpu_idx = out[0].cpu().numpy()
+    sort_ms = 0.0
+    xs = r.xyz
+    if w["sort"]:
+        sort_ms = r.timed(lambda: pcs.sort_axis(r.xyz, w["sort"]), steps)[0] / steps
+        xs = pcs.sort_axis(r.xyz, w["sort"])[0]
+    samp_ms = r.timed(lambda: r.sample_sorted(xs), steps)[0] / steps
+    peak, _ = fp64_peak()
+    hbm, _ = hbm_peak()
+    kern = pcs.kernel_family(w["method"], w["N"], w["M"], w["K"], batch=w["B"])
+    entry = {"ms_per_step": ms, "sampled_pts_per_s": w["B"] * w["C"] / (ms * 1e-3),
+             "clouds_per_s": w["B"] / (ms * 1e-3), "sort_ms": sort_ms, "sampler_ms": samp_ms,
+             "kernel": kern, "dist_evals_per_step": evals,
+             "fp64_frac_algorithmic": (8.0 * evals / (samp_ms * 1e-3) / 1e12 / peak)
+             if peak else None}
+    _, _, _, fp64_pct = ncu_traffic(name)
+    entry["fp64_pipe_executed_frac"] = (fp64_pct / 100.0) if fp64_pct is not None else None
+    if w["sort"]:
+        entry["sort_hbm_frac"] = sort_bytes(w) / (sort_ms * 1e-3) / 1e9 / hbm
+    if kern.startswith("stream"):
+        entry["stream_hbm_frac"] = stream_bytes(w) / (samp_ms * 1e-3) / 1e9 / hbm
+        entry["stream_note"] = "d[] and xyz stay L2-resident (20 B/pt x 1M < 126 MB L2)"
+    e = r.e2e(max(2, steps // 2), 2)
+    e["value"] = w["B"] * w["C"] / (e["ms_per_step"] * 1e-3)
+    e["unit"] = "sampled points/s"
+    entry["e2e"] = e
+    try:
+        cpu, ref_idx, clouds = cpu_reference(w, host_sorted(w, xyz_host), budget_s=cpu_budget_s,
+                                             repeats=2)
+        entry["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        entry["parity"] = parity_of(gpu_idx, ref_idx, clouds)
+        entry["e2e_vs_cpu"] = e["value"] / cpu["value"]
+    except Exception as exc:  # the checker is optional on the box
+        entry["cpu_baseline"] = {"value": None, "sample": f"unavailable: {exc}"}
+    return entry
+
+
+def run_sweep(pcs, torch, dev, names, budget_s, steps=5, warmup=3):
+    """The `workloads` object: every BASELINE config under a wall budget."""
+    out, cache = {}, {}
+    t0 = time.perf_counter()
+    for name in names:
+        if time.perf_counter() - t0 > budget_s:
+            out[name] = {"skipped": f"wall budget of {budget_s:.0f} s spent"}
+            continue
+        w = WORKLOADS[name]
+        key = (w["gen"], w["B"], w["N"])
+        if key not in cache:
+            cache.clear()
+            cache[key] = make_input(w)
+        try:
+            out[name] = measure_workload(pcs, torch, dev, name, w, steps, warmup, cache[key])
+        except Exception as exc:  # keep the sweep going; report the failure
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    out["_wall_s"] = time.perf_counter() - t0
+    return out
 
 
 def main():
@@ -246,6 +543,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-workloads", action="store_true")
+    ap.add_argument("--workloads", default=None,
+                    help="comma-separated subset of the sweep (default: every BASELINE config)")
+    ap.add_argument("--workloads-budget", type=float, default=150.0)
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -255,6 +556,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,173 +566,127 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     args.warmup = max(args.warmup, 3)
-
-    # weak scaling: each rank gets its own clouds (seeded by rank); strong
-    # (one cloud, world > 1): every rank holds the same cloud, sorts it, and
-    # samples its contiguous run of sectors with global index / sector bases
-    strong = bool(w.get("strong")) and world > 1
-    xyz_host = make_input(w, seed_base=0 if strong else 1000 * rank)
-    xyz = torch.from_numpy(xyz_host).to(dev)
     B, N, C = w["B"], w["N"], w["C"]
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    from paper_2208_08795_b200 import shard
 
-    sh = shard.sector_shard(N, C, w["M"], world, rank) if strong else None
-
-    def sample_sorted(xs):
-        if sh is None:
-            return pcs.sample(xs, C, method=w["method"], m=w["M"], k=w["K"])
-        return pcs.sample(xs[:, sh.point_lo:sh.point_hi], sh.c, method=w["method"], m=sh.m,
-                          k=w["K"], index_base=sh.point_lo, sector_base=sh.sector_lo)
-
-    def step(x):
-        if sh is None:
-            return pcs.sample(x, C, method=w["method"], m=w["M"], k=w["K"], sort=w["sort"])
-        xs = pcs.sort_axis(x, w["sort"])[0] if w["sort"] else x
-        return sample_sorted(xs)
+    # strong scaling: the job is the configured batch. Several clouds split
+    # by cloud (BASELINE cfg4: 128 over 8 GPUs = 16 per GPU); one cloud
+    # splits by sector run, every rank sorting the cloud itself
+    mode = "sector" if (B == 1 and world > 1) else "batch"
+    xyz_all = make_input(w)
+    sh = None
+    if mode == "sector":
+        sh = shard.sector_shard(N, C, w["M"], world, rank)
+        xyz_host, b0 = xyz_all, 0
+    else:
+        b0, b1 = shard.split(B, world, rank)
+        xyz_host = np.ascontiguousarray(xyz_all[b0:b1])
+    r = Runner(pcs, torch, dev, w, xyz_host, sh)
 
     for _ in range(args.warmup):
-        out = step(xyz)
+        out = r.step(r.xyz)
     torch.cuda.synchronize()
-    stats = out[1].cpu().numpy()
-    evals_per_step = int(stats[:, 0].sum())
+    evals_local = int(out[1][:, 0].sum().item())
 
     # ---- device-resident throughput (value)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            starts[i].record()
-            step(xyz)
-            ends[i].record()
-        torch.cuda.synchronize()
+        ms, out = r.timed(lambda: r.step(r.xyz), args.steps)
     if world > 1:
         dist.barrier()
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    ms_per_step = ms / args.steps
-    total_samples = B * C if strong else world * B * C
+    ms_per_step = float(t.item()) / args.steps
+    gpu_idx = out[0].cpu().numpy()
+    total_samples = B * C
     pts_per_s = total_samples / (ms_per_step * 1e-3)
 
+    # ---- weak scaling beside it: every rank its own full batch
+    weak = None
+    if world > 1 and mode == "batch":
+        rw = Runner(pcs, torch, dev, w, make_input(w, seed_base=1000 * rank))
+        for _ in range(args.warmup):
+            rw.step(rw.xyz)
+        dist.barrier()
+        wms = rw.timed(lambda: rw.step(rw.xyz), args.steps)[0]
+        t = torch.tensor([wms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wms = float(t.item()) / args.steps
+        weak = {"value": world * B * C / (wms * 1e-3), "unit": "sampled points/s",
+                "ms_per_step": wms, "clouds_per_gpu": B,
+                "note": "every rank samples its own full batch (seeded by rank)"}
+        del rw
+
     # ---- sampler kernel alone (roofline): sort once, time only the sampler
-    xs = pcs.sort_axis(xyz, w["sort"])[0] if w["sort"] else xyz
-    ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern_ms = 0.0
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        ks.record()
-        sample_sorted(xs)
-        ke.record()
-        torch.cuda.synchronize()
-        kern_ms += ks.elapsed_time(ke)
-    kern_ms /= args.steps
+    xs = pcs.sort_axis(r.xyz, w["sort"])[0] if w["sort"] else r.xyz
+    kern_ms = r.timed(lambda: r.sample_sorted(xs), args.steps, per_step_sync=True)[0] / args.steps
     peak, peak_src = fp64_peak()
-    flops = 8.0 * evals_per_step
+    flops = 8.0 * evals_local
     achieved = flops / (kern_ms * 1e-3) / 1e12
-    traffic, traffic_src, ipc = ncu_traffic(args.workload)
+    traffic, traffic_src, ipc, fp64_pct = ncu_traffic(args.workload)
+    kernel = pcs.kernel_family(w["method"], sh.n if sh else N, sh.m if sh else w["M"], w["K"],
+                               batch=xyz_host.shape[0])
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                "frac": (achieved / peak) if peak else None,
+                "traffic": traffic if world == 1 and mode == "batch" else None,
                 "traffic_source": traffic_src,
                 # what actually limits the serial update->argmax->pivot chain:
                 # issued instructions per SM-cycle (ncu) against the 4 schedulers
                 "issue": ({"ipc_per_sm": ipc, "peak_ipc": 4.0, "frac": ipc / 4.0}
                           if ipc else None),
-                "algorithmic_hbm_bytes": B * N * 12 + B * C * 4,
-                "kernel": pcs.kernel_family(w["method"], N, w["M"], w["K"], batch=B),
-                "kernel_ms": kern_ms, "algorithmic_flops": flops, "peak_source": peak_src,
-                "note": "FP64 flops = 8 x dist_evals (3 sub, 3 mul, 2 add; no FMA); the "
-                        "argmax work is not counted"}
+                "fp64_pipe_executed_frac": (fp64_pct / 100.0) if fp64_pct is not None else None,
+                "algorithmic_hbm_bytes": xyz_host.shape[0] * N * 12 + xyz_host.shape[0] * C * 4,
+                "kernel": kernel, "kernel_ms": kern_ms, "algorithmic_flops": flops,
+                "peak_source": peak_src,
+                "note": "FP64 flops = 8 x dist_evals (3 sub, 3 mul, 2 add; no FMA) of this "
+                        "rank's launch; the argmax work is not counted; kernel_ms = CUDA "
+                        "events on the launching stream, synchronised per launch"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        pinned = torch.from_numpy(xyz_host).pin_memory()
+        e2e = r.e2e(args.steps, args.warmup, world, dist if world > 1 else None)
+        e2e["value"] = total_samples / (e2e["ms_per_step"] * 1e-3)
+        e2e["unit"] = "sampled points/s"
 
-        def e2e_step():
-            # the C-ABI host-buffer entry (pcs_sample_host_batch, through
-            # pcs.sample_host_batch): pinned batch in, host results out,
-            # chunked H2D / sort + sample / D2H inside the native call
-            if sh is None:
-                return pcs.sample_host_batch(pinned, C, method=w["method"], m=w["M"], k=w["K"],
-                                             sort=w["sort"])
-            res = step(pinned.to(dev, non_blocking=True))
-            return tuple(t.cpu() for t in res)
-
-        # warm-up: at least W steps and 0.5 s -- the host link ramps up over
-        # the first ~15 transfers after idling (1.6-3 ms -> 1.2 ms per step
-        # measured, tools/e2e_dbg.py)
-        t_warm = time.perf_counter()
-        for i in range(max(args.warmup, 1000)):
-            e2e_step()
-            if i + 1 >= args.warmup and time.perf_counter() - t_warm > 0.5:
-                break
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_ms = 0.0
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            es.record()
-            e2e_step()
-            ee.record()
-            torch.cuda.synchronize()
-            e_ms += es.elapsed_time(ee)
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item()) / args.steps
-        r = e2e_step()
-        # the PCIe floor on this box: one plain H2D of the same pinned batch
-        dst = torch.empty(pinned.shape, dtype=pinned.dtype, device=dev)
-        h2d = []
-        for _ in range(5):
-            es.record()
-            dst.copy_(pinned, non_blocking=True)
-            ee.record()
-            torch.cuda.synchronize()
-            h2d.append(es.elapsed_time(ee))
-        del dst
-        e2e = {"value": total_samples / (e_ms * 1e-3), "unit": "sampled points/s",
-               "ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
-               "h2d_gbps": pinned.numel() * pinned.element_size() / min(h2d) / 1e6,
-               "h2d_bytes_per_step": int(pinned.numel() * pinned.element_size()),
-               "d2h_bytes_per_step": int(sum(t.nbytes if hasattr(t, "nbytes") else
-                                             t.numel() * t.element_size() for t in r)),
-               "path": ("C-ABI pcs_sample_host_batch (pinned host tensor in, host arrays out): "
-                        "chunked H2D overlapped with sort+sample, D2H of indices, stats (and "
-                        "perm when sorting)") if sh is None else
-                       "pinned H2D, sort, sample of this rank's sectors, D2H"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # ---- reference on the host: baseline (N=1) and parity (rank 0's clouds)
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference(w, host_sorted(w, xyz_host))
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+            res, ref_idx, clouds = cpu_reference(
+                w, host_sorted(w, xyz_host if mode == "batch" else xyz_all))
+            if world == 1:
+                cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                            "cpu_model")}
+            if mode == "batch":
+                parity = parity_of(gpu_idx, ref_idx, clouds)
+            else:  # rank 0's sectors are the first out slots of the cloud
+                c0 = min(gpu_idx.shape[1], ref_idx.shape[1])
+                parity = parity_of(gpu_idx[:, :c0], ref_idx[:, :c0], clouds)
         except Exception as exc:  # the checker is optional on the box
             cpu = {"value": None, "unit": "sampled points/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
+
+    sweep = None
+    if world == 1 and not args.no_workloads:
+        names = args.workloads.split(",") if args.workloads else SWEEP
+        sweep = run_sweep(pcs, torch, dev, names, args.workloads_budget)
 
     if rank == 0:
         line = {
             "metric": "sampled points/s", "value": pts_per_s, "unit": "sampled points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if strong else "weak",
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "clouds_per_s": (B if strong else world * B) / (ms_per_step * 1e-3),
-            "config": arm_config(args.workload, w, world, strong),
+            "clouds_per_s": B / (ms_per_step * 1e-3),
+            "config": arm_config(args.workload, w, world, mode),
             "gpu_launches": args.steps * launches_per_step(w),
-            "dist_evals_per_step": evals_per_step,
-            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
-            "clocks": clocks.summary(),
+            "dist_evals_per_step_rank0": evals_local,
+            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+            "weak": weak, "clocks": clocks.summary(), "workloads": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -176,6 +176,16 @@ int pcs_separation_host(const double* xyz, int64_t n, const int64_t* samples, in
 long long pcs_read_cloud_host(const char* path, int32_t format, double* out_xyz, int64_t capacity);
 int pcs_write_cloud_host(const char* path, int32_t format, const double* xyz, int64_t n);
 
+/* The kernel pcs_gpu_sample would launch for `args` (batch, n, c, m, k,
+ * method, coord_dtype and trace-free; pointers are ignored), e.g.
+ * "npdu_tmem_kernel<5,1024>", written NUL-terminated into name[capacity].
+ * Touches no device. Validation errors as pcs_gpu_sample. */
+int pcs_kernel_family(const pcs_gpu_args* args, char* name, size_t capacity);
+
+/* Test hook: re-read the PCS_* engine-override environment variables, which
+ * are otherwise read once per process. */
+void pcs_debug_reload_knobs(void);
+
 /* Last error message of the calling thread ("" after success). */
 const char* pcs_last_error(void);
 const char* pcs_status_string(int status);

@@ -3,7 +3,9 @@
 // reference-facing bindings call.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -15,24 +17,58 @@
 namespace pcs_internal {
 
 cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t st) {
-  static std::atomic<unsigned long long> retained{0};  // bit per device (< 64)
+  // one private stream-ordered pool per device (< 64), created on first use:
+  // it keeps freed workspace mapped for the next call (release threshold =
+  // max) without changing the behaviour of the device's default pool, which
+  // the caller's allocator (e.g. torch) may use
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
-  if (bit && !(retained.load() & bit)) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, st);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) {
+        pools[dev] = nullptr;
+        return e;
+      }
       unsigned long long keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    retained.fetch_or(bit);
+    pool = pools[dev];
   }
-  return cudaMallocAsync(p, bytes, st);
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
 }
 
 namespace {
 thread_local std::string g_error;
+
+Knobs read_knobs() {
+  Knobs k;
+  auto env = [](const char* name) -> const char* { return std::getenv(name); };
+  if (const char* v = env("PCS_SAMPLER")) k.sampler = std::string(v) == "rows" ? 1 : std::string(v) == "stream" ? 2 : 0;
+  if (const char* v = env("PCS_MORTON")) k.morton = v[0] != '0';
+  if (const char* v = env("PCS_MORTON_TMEM")) k.morton_tmem = v[0] != '0';
+  if (const char* v = env("PCS_MORTON_MIN")) k.morton_min = std::atoll(v);
+  if (const char* v = env("PCS_NPDU_WIDE")) k.npdu_wide = std::atoll(v);
+  if (const char* v = env("PCS_NPDU_TMEM")) k.npdu_tmem = v[0] != '0';
+  if (const char* v = env("PCS_NPDU_BIG")) k.npdu_big = v[0] != '0';
+  if (const char* v = env("PCS_SORT_RADIX")) k.sort_radix = v[0] != '0';
+  return k;
+}
+
+// Snapshots are immutable and never freed (a reload is a test-only event),
+// so a launch racing a reload reads either snapshot, never a torn one.
+std::atomic<const Knobs*> g_knobs{nullptr};
 
 const char* who(int method) {
   switch (method) {
@@ -67,6 +103,18 @@ struct DevBuf {
 };
 
 }  // namespace
+
+const Knobs& knobs() {
+  const Knobs* k = g_knobs.load(std::memory_order_acquire);
+  if (!k) {
+    const Knobs* fresh = new Knobs(read_knobs());
+    if (!g_knobs.compare_exchange_strong(k, fresh, std::memory_order_acq_rel)) delete fresh;
+    else k = fresh;
+  }
+  return *k;
+}
+
+void reload_knobs() { g_knobs.store(new Knobs(read_knobs()), std::memory_order_release); }
 
 void set_error(const std::string& msg) { g_error = msg; }
 void clear_error() { g_error.clear(); }
@@ -137,6 +185,24 @@ int pcs_gpu_sample(const pcs_gpu_args* a, void* stream) {
   const cudaError_t e = launch_sample(*a, static_cast<cudaStream_t>(stream), &msg);
   return e == cudaSuccess ? PCS_OK : cuda_fail(e, msg);
 }
+
+int pcs_kernel_family(const pcs_gpu_args* a, char* name, size_t capacity) {
+  clear_error();
+  if (!a) { set_error("pcs_kernel_family: null args"); return PCS_ERR_INVALID_ARGUMENT; }
+  std::string msg;
+  const int rc = validate_sample(a->method, a->n, a->c, a->m, a->k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  std::string plan;
+  if (plan_sample(*a, &plan, &msg) != 0) { set_error(msg); return PCS_ERR_UNSUPPORTED; }
+  if (name && capacity) {
+    const size_t len = std::min(capacity - 1, plan.size());
+    std::memcpy(name, plan.data(), len);
+    name[len] = '\0';
+  }
+  return PCS_OK;
+}
+
+void pcs_debug_reload_knobs(void) { reload_knobs(); }
 
 int pcs_gpu_sort_axis(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
                       int32_t axis, void* out_xyz, int32_t* out_perm, void* stream) {
@@ -439,6 +505,8 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
   clear_error();
   if (axis < 0 || axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
   if (n <= 0) return PCS_OK;
+  // int32 permutation and 32-bit sort indices on every path
+  if (n > 0x7fffffffLL) { set_error("clouds above 2^31-1 points are not supported"); return PCS_ERR_UNSUPPORTED; }
   DevStreams* dsp = nullptr;
   cudaError_t e = device_streams(&dsp);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -451,7 +519,7 @@ int pcs_exact_sort_host(const double* xyz, int64_t n, int32_t axis, double* out_
   // operator< order (fp32 widens exactly; -0.0 folds onto +0.0 either way),
   // a third of the copy, the on-chip fp32 sort kernels; only the permutation
   // comes back and the host gathers the float64 points through it.
-  bool f32_keys = n <= 0x7fffffffLL;
+  bool f32_keys = true;
   for (int64_t i = 0; i < n && f32_keys; ++i) {
     const double v = xyz[3 * i + axis];
     f32_keys = static_cast<double>(static_cast<float>(v)) == v;  // NaN: not exact

@@ -251,10 +251,12 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
 }
 
 template <typename Kern>
-cudaError_t launch_groups(Kern kern, SampleParams p, int W, int G, cudaStream_t st) {
+cudaError_t launch_groups(Kern kern, const char* name, std::initializer_list<long long> targs,
+                          SampleParams p, int W, int G, cudaStream_t st) {
   const size_t group_bytes = size_t(24) * p.nmax + 32 * W;
   const size_t smem = group_bytes * G;
   if (smem > kMaxSmem) return cudaErrorInvalidConfiguration;
+  if (plan(name, targs)) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -279,7 +281,7 @@ int pick_groups(long long sectors, int W, int nmax, int max_threads) {
 template <int P, int W, bool REGC>
 cudaError_t run_full(SampleParams p, cudaStream_t st) {
   const int G = pick_groups(p.B * p.M, W, p.nmax, W >= 8 ? W * 32 : 256);
-  return launch_groups(fps_full_kernel<P, W, REGC>, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
+  return launch_groups(fps_full_kernel<P, W, REGC>, "fps_full_kernel", {P, W, REGC}, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
 }
 
 cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
@@ -296,11 +298,9 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   // 8 slots per thread (twice the warps, ~120 registers) hides more latency
   // when an SM holds one sector or at least four; with ~2 sectors per SM the
   // 16-slot form measured faster (r01 sweep: cfg5 FPS 2K 0.374 vs 0.400 ms;
-  // AFPS M=4 at 8K 1.69 vs 1.33 ms, cfg1 0.283 vs 0.262 ms). PCS_FULL_P
-  // (8 or 16) overrides.
+  // AFPS M=4 at 8K 1.69 vs 1.33 ms, cfg1 0.283 vs 0.262 ms).
   const long long sectors = p.B * p.M;
-  bool p8 = sectors >= 4 * 148 || sectors <= 148;
-  if (const char* pe = std::getenv("PCS_FULL_P")) p8 = std::atoi(pe) == 8;
+  const bool p8 = sectors >= 4 * 148 || sectors <= 148;
   if (p8) {
     if (n <= 512) return run_full<8, 2, true>(p, st);
     if (n <= 1024) return run_full<8, 4, true>(p, st);
@@ -318,7 +318,7 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
 template <int P, int W>
 cudaError_t run_wide(SampleParams p, cudaStream_t st) {
   const int G = pick_groups(p.B * p.M, W, p.nmax, W >= 8 ? W * 32 : 256);
-  return launch_groups(npdu_wide_kernel<P, W>, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
+  return launch_groups(npdu_wide_kernel<P, W>, "npdu_wide_kernel", {P, W}, p, W, std::min(G, W >= 8 ? 1 : 8 / W), st);
 }
 
 // Windowed sectors <= 4096 points, W >= 8 warps (a window of <= 8 rows -- k

@@ -25,6 +25,10 @@ int validate_sample(int method, int64_t n, int64_t c, int64_t m, int64_t k, std:
 // Enqueues the batched sampler (args already validated). Zeroes out_stats.
 cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::string* msg);
 
+// The kernel launch_sample would make for `a` (no device work): 0 and its
+// name (e.g. "npdu_tmem_kernel<5,1024>"), or -1 with *msg when none fits.
+int plan_sample(const pcs_gpu_args& a, std::string* name, std::string* msg);
+
 // Enqueues the batched stable axis sort.
 cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t n, int axis,
                         void* out_xyz, int32_t* out_perm, cudaStream_t stream);
@@ -41,6 +45,22 @@ cudaError_t launch_local_fps(const double* xyz, int64_t n, int64_t sb, int64_t s
 cudaError_t launch_metric(int which, int coord_dtype, const void* xyz, int64_t batch, int64_t n,
                           int index_dtype, const void* idx, int64_t c, double* out,
                           cudaStream_t stream);
+
+// Engine-selection overrides for tests and A/B measurements, read from the
+// environment ONCE per process (never per launch); pcs_debug_reload_knobs()
+// re-reads them (test hook).
+struct Knobs {
+  int sampler = 0;            // PCS_SAMPLER: 0 auto, 1 "rows" (pruned rows), 2 "stream"
+  bool morton = true;         // PCS_MORTON=0: storage-order rows instead of Morton rows
+  bool morton_tmem = true;    // PCS_MORTON_TMEM=0: Morton rows keep d in shared memory
+  long long morton_min = -1;  // PCS_MORTON_MIN: full-window Morton crossover (points)
+  long long npdu_wide = -1;   // PCS_NPDU_WIDE: most sectors the W-warp NPDU form takes
+  bool npdu_tmem = true;      // PCS_NPDU_TMEM=0: one-warp NPDU keeps d in shared memory
+  bool npdu_big = true;       // PCS_NPDU_BIG=0: no TMEM row engine for big windowed sectors
+  bool sort_radix = true;     // PCS_SORT_RADIX=0: bitonic networks instead of on-chip radix
+};
+const Knobs& knobs();
+void reload_knobs();
 
 void set_error(const std::string& msg);
 void clear_error();

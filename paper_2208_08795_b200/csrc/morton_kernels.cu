@@ -498,6 +498,7 @@ cudaError_t launch_morton(SampleParams p, int np, cudaStream_t st) {
   p.nmax = np;
   const size_t smem = morton_smem_bytes<CT>(np, W, CS);
   if (smem > kMaxSmem) return cudaErrorNotSupported;
+  if (plan("morton_rows_kernel", {sizeof(CT), W, CS})) return cudaSuccess;
   auto kern = morton_rows_kernel<CT, W, CS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -525,12 +526,9 @@ cudaError_t launch_morton(SampleParams p, int np, cudaStream_t st) {
 
 // Warps per CTA: one row per lane, so W >= rows / 32. Morton rows leave far
 // fewer rows to update per iteration than slab rows, so the fixed per-warp
-// reduction cost argues for the smallest W that holds the rows
-// (PCS_MORTON_W overrides for tuning).
+// reduction cost argues for the smallest W that holds the rows.
 int morton_w(int rows) {
-  int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
-  if (const char* e = std::getenv("PCS_MORTON_W")) w = std::max(w, std::atoi(e));
-  return w > 8 ? 16 : w;
+  return rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
 }
 
 template <typename CT, int CS>

@@ -512,6 +512,7 @@ cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
   int cols = 32;
   while (cols < W * rpw) cols *= 2;  // W/4 warps per quarter x 4 columns x rpw rows
   if (cols > 512) return cudaErrorNotSupported;
+  if (plan("morton_tmem_kernel", {W, CS, WIN})) return cudaSuccess;
   auto kern = morton_tmem_kernel<W, CS, WIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -540,14 +541,10 @@ cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
 // Warps per CTA: the fewest that give one row per lane, except that CTAs
 // of 65-128 rows get 8 warps when the SMs hold about two sectors or fewer
 // (r01: 256 x 4K FPS 1.24 -> 1.13 ms; with ~7 sectors per SM the smaller
-// CTAs win: AFPS M=4 at 8K 1.09 vs 1.37 ms). PCS_MORTON_TMEM_W overrides.
+// CTAs win: AFPS M=4 at 8K 1.09 vs 1.37 ms).
 int morton_tmem_w(int rows, long long sectors) {
   int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
   if (w == 4 && rows > 64 && sectors <= 2 * 148) w = 8;
-  if (const char* e = std::getenv("PCS_MORTON_TMEM_W")) {
-    const int v = std::atoi(e);
-    if (v == 4 || v == 8 || v == 16) w = std::max(w, v);
-  }
   return w;
 }
 
@@ -568,21 +565,14 @@ cudaError_t launch_morton_tmem_w(SampleParams p, int rows, cudaStream_t st) {
 
 }  // namespace
 
-// Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory),
-// at least cs_min CTAs for batches of few sectors.
-constexpr int kMortonSpreadMax = 1;
+// Smallest cluster whose per-CTA share fits (<= 512 rows and shared memory).
+// (Spreading few sectors over larger clusters than capacity needs measured
+// slower everywhere but a lone 32K cloud.)
 cudaError_t run_morton_tmem_any(SampleParams p, long long n, cudaStream_t st) {
   // fp32 batches; distance traces come from the fp64 drop-in (other engines)
   if (p.f64 || p.trace) return cudaErrorNotSupported;
   const long long srows = (n + 31) / 32;
-  // Few sectors: spread each over more SMs (a larger cluster) while the
-  // batch still fits one CTA per SM -- the per-iteration row work shrinks
-  // with the CTA's share. PCS_MORTON_CS_MIN overrides (A/B).
-  int cs_min = 1;
-  const long long sectors = p.B * p.M;
-  while (cs_min < kMortonSpreadMax && sectors * cs_min * 2 <= 148 && srows >= 64LL * cs_min * 2)
-    cs_min *= 2;
-  if (const char* e = std::getenv("PCS_MORTON_CS_MIN")) cs_min = std::max(1, std::atoi(e));
+  const int cs_min = 1;
   for (int CS = cs_min; CS <= 16; CS *= 2) {
     const int rows = static_cast<int>((srows + CS - 1) / CS);
     if (rows > 512) continue;

@@ -283,6 +283,7 @@ cudaError_t run_npdu(SampleParams p, cudaStream_t st) {
   const int G = static_cast<int>(std::max(1LL, std::min({24LL, per_sm, sectors / 148})));
   const size_t smem = warp_bytes * G;
   if (smem > kMaxSmem) return cudaErrorNotSupported;
+  if (plan("npdu_warp_kernel", {sizeof(CT), RPL, RMAX, GC})) return cudaSuccess;
   auto kern = npdu_warp_kernel<CT, RPL, RMAX, GC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -305,11 +306,6 @@ cudaError_t run_npdu_rows(SampleParams p, cudaStream_t st) {
 
 template <int RPL>
 cudaError_t run_npdu_rpl(SampleParams p, cudaStream_t st) {
-  const char* gc = std::getenv("PCS_NPDU_GC");
-  if (gc && gc[0] == '1') {
-    if (p.f64) return run_npdu_rows<double, RPL, true>(p, st);
-    return run_npdu_rows<float, RPL, true>(p, st);
-  }
   if (p.f64) return run_npdu_rows<double, RPL, false>(p, st);
   // fp32 input: stage fp32 (widened exactly on use) unless fp64 staging
   // still fits 16 warps per SM
@@ -606,11 +602,11 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
     G = 4;
   else
     G = std::max(1LL, std::min(G, (sectors + 148 * waves - 1) / (148 * waves)));
-  if (const char* ge = std::getenv("PCS_NPDU_G")) G = std::max(1, std::atoi(ge));  // A/B knob
   int cols = 32;
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
   const size_t smem = wsm * G;
+  if (plan("npdu_tmem_kernel", {RMAX, NCAP})) return cudaSuccess;
   auto kern = npdu_tmem_kernel<RMAX, NCAP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -626,14 +622,13 @@ cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
   // limit, and the W-warp register kernel (full_kernels.cu) runs it ~18%
   // shorter than one warp per sector. PCS_NPDU_WIDE = the largest batch (in sectors) that
   // takes it (0 disables).
-  long long wide_max = kNpduWideMax;
-  if (const char* wv = std::getenv("PCS_NPDU_WIDE")) wide_max = std::atoll(wv);
+  const pcs_internal::Knobs& kn = pcs_internal::knobs();
+  const long long wide_max = kn.npdu_wide >= 0 ? kn.npdu_wide : kNpduWideMax;
   if (p.B * p.M <= wide_max && n <= 4096) {
     const cudaError_t e = run_npdu_wide_any(p, n, st);
     if (e != cudaErrorNotSupported) return e;
   }
-  const char* tmv = std::getenv("PCS_NPDU_TMEM");
-  const bool use_tmem = !(tmv && tmv[0] == '0');
+  const bool use_tmem = kn.npdu_tmem;
   const long long rows_needed = (p.K + 62) / 32;
   // (the TMEM kernel serves fp32 batches; distance traces come from the
   // fp64 drop-in and take the shared-memory kernels)

@@ -292,6 +292,25 @@ PYBIND11_MODULE(_core, m) {
         py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
         py::arg("out_stats"), py::arg("stream"), py::arg("index_base") = 0,
         py::arg("sector_base") = 0);
+  // the dispatch decision of pcs_gpu_sample (no device work)
+  m.def("kernel_family",
+        [](int method, int coord_dtype, std::int64_t batch, std::int64_t n, std::int64_t c,
+           std::int64_t mm, std::int64_t k) {
+          pcs_gpu_args a{};
+          a.method = method;
+          a.coord_dtype = coord_dtype;
+          a.batch = batch;
+          a.n = n;
+          a.c = c;
+          a.m = mm;
+          a.k = k;
+          char name[128];
+          check(pcs_kernel_family(&a, name, sizeof(name)));
+          return std::string(name);
+        },
+        py::arg("method"), py::arg("coord_dtype"), py::arg("batch"), py::arg("n"), py::arg("c"),
+        py::arg("m"), py::arg("k"));
+  m.def("reload_knobs", []() { pcs_debug_reload_knobs(); });
   // the host-buffer batch entry (pointers into host memory, e.g. pinned
   // torch tensors); the GIL is released for the synchronous call
   m.def("sample_host_ptr",

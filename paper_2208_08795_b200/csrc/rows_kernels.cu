@@ -386,6 +386,7 @@ cudaError_t launch_rows(SampleParams p, int chunk, cudaStream_t st) {
   p.nmax = chunk;
   const size_t smem = rows_smem_bytes<CT>(chunk, W, CS);
   if (smem > kMaxSmem) return cudaErrorNotSupported;
+  if (plan("rows_kernel", {sizeof(CT), W, RPL, CS, WIN})) return cudaSuccess;
   auto kern = rows_kernel<CT, W, RPL, CS, WIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));

@@ -1,5 +1,5 @@
 // Batched sampler entry: picks the kernel family per sector size and window.
-#include <cstdlib>
+#include <initializer_list>
 
 #include "sampler_common.cuh"
 
@@ -16,40 +16,48 @@ constexpr long long kMortonMin = 3072;
 constexpr long long kMortonMinBusy = 1024;
 constexpr long long kBusySectors = 4 * 148;
 
+thread_local std::string* g_plan = nullptr;
+
+std::string kname(const char* base, std::initializer_list<long long> args) {
+  std::string s(base);
+  s += '<';
+  bool first = true;
+  for (long long a : args) {
+    if (!first) s += ',';
+    s += std::to_string(a);
+    first = false;
+  }
+  return s + '>';
+}
+
 cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaStream_t st,
                      std::string* msg) {
   p.nmax = static_cast<int>((nmax_sector + 1) & ~1LL);
-  // PCS_SAMPLER=rows forces the pruned-row engine (benchmarking / tests)
-  const char* force = std::getenv("PCS_SAMPLER");
-  const bool rows = force && std::string(force) == "rows";
-  // PCS_SAMPLER=stream forces the streaming engine (tests)
-  if (force && std::string(force) == "stream") return run_stream_any(p, nmax_sector, st);
+  const pcs_internal::Knobs& kn = pcs_internal::knobs();
+  // PCS_SAMPLER=rows forces the pruned-row engine, =stream the streaming
+  // engine (tests, A/B)
+  const bool rows = kn.sampler == 1;
+  if (kn.sampler == 2) return run_stream_any(p, nmax_sector, st);
   // full-window sectors: Morton rows beyond the register kernels' sweet
-  // spot (PCS_MORTON=0 selects the storage-order rows, for A/B and tests;
-  // PCS_MORTON_MIN moves the crossover)
-  const char* morton = std::getenv("PCS_MORTON");
-  const bool use_morton = !windowed && !(morton && std::string(morton) == "0");
-  const char* mmin = std::getenv("PCS_MORTON_MIN");
-  const long long morton_min = mmin ? std::atoll(mmin) : kMortonMin;
+  // spot (PCS_MORTON=0 selects the storage-order rows, PCS_MORTON_MIN moves
+  // the crossover)
+  const bool use_morton = !windowed && kn.morton;
+  const long long morton_min = kn.morton_min >= 0 ? kn.morton_min : kMortonMin;
   // fp32 input: the TMEM form first (per-point state in tensor memory, half
   // the shared memory per point); PCS_MORTON_TMEM=0 keeps it in shared memory
-  const char* mt = std::getenv("PCS_MORTON_TMEM");
-  const bool morton_tmem = !p.f64 && !(mt && std::string(mt) == "0");
+  const bool morton_tmem = !p.f64 && kn.morton_tmem;
   auto morton_any = [&]() {
     cudaError_t r = morton_tmem ? run_morton_tmem_any(p, nmax_sector, st) : cudaErrorNotSupported;
     return r == cudaErrorNotSupported ? run_morton_any(p, nmax_sector, st) : r;
   };
-  const bool busy = p.B * p.M >= kBusySectors && nmax_sector > kMortonMinBusy && !mmin;
+  const bool busy = p.B * p.M >= kBusySectors && nmax_sector > kMortonMinBusy && kn.morton_min < 0;
   cudaError_t e = cudaErrorNotSupported;
   if (use_morton && (rows || nmax_sector > morton_min || (busy && morton_tmem))) e = morton_any();
   // windowed sectors past the TMEM NPDU kernel (> 4096 points, fp32): the
   // TMEM row engine in storage order, rows restricted to the window
   // (PCS_NPDU_BIG=0 keeps the warp / shared-memory row kernels)
-  const char* nb = std::getenv("PCS_NPDU_BIG");
-  const char* nbm = std::getenv("PCS_NPDU_BIG_MIN");  // A/B: crossover (points per sector)
-  const long long big_min = nbm ? std::atoll(nbm) : 4096;
-  if (e == cudaErrorNotSupported && !rows && windowed && !p.f64 && nmax_sector > big_min &&
-      !(nb && std::string(nb) == "0"))
+  if (e == cudaErrorNotSupported && !rows && windowed && !p.f64 && nmax_sector > 4096 &&
+      kn.npdu_big)
     e = run_morton_tmem_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && !rows)
     e = windowed ? run_npdu_any(p, nmax_sector, st) : run_full_any(p, nmax_sector, st);
@@ -67,11 +75,13 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
 
 namespace pcs_internal {
 
-cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::string* msg) {
+namespace {
+
+pcsk::SampleParams params_of(const pcs_gpu_args& a, long long* nmax) {
   const bool sectored = a.method == PCS_METHOD_AFPS || a.method == PCS_METHOD_NPDU_AFPS;
   const bool windowed = a.method == PCS_METHOD_NPDU_FPS || a.method == PCS_METHOD_NPDU_AFPS;
   const long long M = sectored ? a.m : 1;
-  const long long nmax = (a.n + M - 1) / M;
+  *nmax = (a.n + M - 1) / M;
   pcsk::SampleParams p{};
   p.xyz = a.xyz;
   p.f64 = a.coord_dtype == PCS_DTYPE_F64;
@@ -82,7 +92,7 @@ cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::strin
   // A window that always covers the whole sector is the full update
   // (k >= 2*n-1 => update_window == sector for every pivot), and the
   // OpStats agree: every window then holds the sector's n points.
-  p.K = (windowed && a.k < 2 * nmax - 1) ? a.k : 0;
+  p.K = (windowed && a.k < 2 * *nmax - 1) ? a.k : 0;
   p.random_first = a.seed_policy == PCS_RANDOM_FIRST_POINT;
   p.seed = a.seed;
   p.seeds = a.seeds;
@@ -92,11 +102,28 @@ cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::strin
   p.stats = reinterpret_cast<unsigned long long*>(a.out_stats);
   p.index_base = a.index_base;
   p.sector_base = a.sector_base;
+  return p;
+}
+
+}  // namespace
+
+cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::string* msg) {
+  long long nmax = 0;
+  const pcsk::SampleParams p = params_of(a, &nmax);
   if (a.out_stats) {
     cudaError_t e = cudaMemsetAsync(a.out_stats, 0, sizeof(uint64_t) * 4 * a.batch, stream);
     if (e != cudaSuccess) return e;
   }
   return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+}
+
+int plan_sample(const pcs_gpu_args& a, std::string* name, std::string* msg) {
+  long long nmax = 0;
+  const pcsk::SampleParams p = params_of(a, &nmax);
+  pcsk::g_plan = name;
+  const cudaError_t e = pcsk::dispatch(p, nmax, p.K > 0, nullptr, msg);
+  pcsk::g_plan = nullptr;
+  return e == cudaSuccess ? 0 : -1;
 }
 
 cudaError_t launch_local_fps(const double* xyz, int64_t n, int64_t sb, int64_t se,

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <initializer_list>
 #include <string>
 
 #include "device_common.cuh"
@@ -206,6 +207,18 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // 0.117 vs 0.142 ms; at 256 sectors the one-warp TMEM kernel wins again
 // (0.141 vs 0.152 ms) and at 512 by 2x (tools/npdu_wide_ab.py)
 constexpr long long kNpduWideMax = 148;
+
+// Plan mode (pcs_kernel_family): while set, the launchers store the name of
+// the kernel they would launch here and return cudaSuccess without touching
+// the device. The check sits right before each launch, after every fit
+// test, so the plan is the dispatch decision itself.
+extern thread_local std::string* g_plan;
+std::string kname(const char* base, std::initializer_list<long long> args);
+inline bool plan(const char* base, std::initializer_list<long long> args) {
+  if (!g_plan) return false;
+  *g_plan = kname(base, args);
+  return true;
+}
 
 // Launchers (one per translation unit). They return cudaErrorNotSupported
 // when the sector does not fit the kernel family.

@@ -384,194 +384,9 @@ cudaError_t launch_reg_sort(const float* xyz, long long batch, long long n, int 
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- large clouds
-// Bitonic network on packed (orderkey << 32 | index) words, extended past one
-// CTA's shared memory: a cluster of CS CTAs holds CS blocks of kBlk words
-// (clouds up to 16 x 16384 = 262144 points, DSMEM for the steps whose partner
-// is in another CTA), or for larger clouds the words live in global (L2)
-// memory, with block-local steps in shared memory and one launch per global
-// step. Direction of every compare-exchange: ascending iff (i & k) == 0 for
-// the global index i, so all variants compute the same network.
-
+// Cluster size unit of the register networks (launch_reg_sort<16, CS>):
+// one CTA holds 16384 keys.
 constexpr int kBlk = 16384;
-
-__device__ __forceinline__ unsigned long long pack_word(const float* __restrict__ src, long long N,
-                                                        long long i, int axis) {
-  return i < N ? (static_cast<unsigned long long>(order_key(src[3 * i + axis])) << 32) |
-                     static_cast<unsigned>(i)
-               : ~0ull;
-}
-
-// steps j = j0, j0/2, ..., 1 of stage k over a block of `len` words that
-// starts at global index `base`
-__device__ __forceinline__ void block_steps(unsigned long long* w, int len, long long base,
-                                            long long k, int j0) {
-  for (int j = j0, lj = __ffs(j0) - 1; j > 0; j >>= 1, --lj) {
-    for (int i = threadIdx.x; i < len / 2; i += blockDim.x) {
-      const int lo = ((i >> lj) << (lj + 1)) | (i & (j - 1)), hi = lo + j;
-      const unsigned long long a = w[lo], c = w[hi];
-      if ((a > c) == (((base + lo) & k) == 0)) {
-        w[lo] = c;
-        w[hi] = a;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ void block_sort(unsigned long long* w, int len, long long base) {
-  for (long long k = 2; k <= len; k <<= 1) block_steps(w, len, base, k, static_cast<int>(k >> 1));
-}
-
-template <int CS>
-__global__ void __launch_bounds__(kSortThreads)
-    bitonic_cluster_kernel(const float* __restrict__ xyz, long long N, int axis,
-                           float* __restrict__ out_xyz, int* __restrict__ out_perm) {
-  extern __shared__ __align__(16) unsigned long long words[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = static_cast<int>(cluster.block_rank());
-  const long long b = blockIdx.x / CS;
-  const long long base = static_cast<long long>(rank) * kBlk;
-  const long long T = static_cast<long long>(CS) * kBlk;
-  const float* src = xyz + b * N * 3;
-  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) words[i] = pack_word(src, N, base + i, axis);
-  __syncthreads();
-  block_sort(words, kBlk, base);
-  for (long long k = 2LL * kBlk; k <= T; k <<= 1) {
-    long long j = k >> 1;
-    for (; j >= kBlk; j >>= 1) {
-      cluster.sync();
-      const int partner = rank ^ static_cast<int>(j / kBlk);
-      if (rank < partner) {
-        unsigned long long* remote = cluster.map_shared_rank(words, partner);
-        for (int i = threadIdx.x; i < kBlk; i += kSortThreads) {
-          const unsigned long long a = words[i], c = remote[i];
-          if ((a > c) == (((base + i) & k) == 0)) {
-            words[i] = c;
-            remote[i] = a;
-          }
-        }
-      }
-    }
-    cluster.sync();
-    block_steps(words, kBlk, base, k, kBlk / 2);
-  }
-  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
-  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) {
-    const long long g = base + i;
-    if (g < N) {
-      const int from = static_cast<int>(words[i] & 0xffffffffu);
-      if (out_perm) out_perm[b * N + g] = from;
-      if (dst) gather_point(src, dst, g, from);
-    }
-  }
-  cluster.sync();  // no CTA leaves while a partner may still touch its words
-}
-
-__global__ void pack_kernel(const float* __restrict__ xyz, long long N, long long T, int axis,
-                            unsigned long long* __restrict__ keys) {
-  const long long b = blockIdx.y;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < T; i += 256LL * gridDim.x)
-    keys[b * T + i] = pack_word(xyz + b * N * 3, N, i, axis);
-}
-
-// one CTA per kBlk block: either the full block sort (k0 == 0) or the local
-// steps kBlk/2..1 of stage k0
-__global__ void __launch_bounds__(kSortThreads)
-    block_kernel(unsigned long long* keys, long long T, long long k0) {
-  extern __shared__ __align__(16) unsigned long long words[];
-  const long long b = blockIdx.y;
-  const long long base = static_cast<long long>(blockIdx.x) * kBlk;
-  unsigned long long* g = keys + b * T + base;
-  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) words[i] = g[i];
-  __syncthreads();
-  if (k0 == 0)
-    block_sort(words, kBlk, base);
-  else
-    block_steps(words, kBlk, base, k0, kBlk / 2);
-  for (int i = threadIdx.x; i < kBlk; i += kSortThreads) g[i] = words[i];
-}
-
-__global__ void global_step_kernel(unsigned long long* keys, long long T, long long k, long long j) {
-  const long long b = blockIdx.y;
-  unsigned long long* w = keys + b * T;
-  const int lj = __ffsll(j) - 1;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < T / 2; i += 256LL * gridDim.x) {
-    const long long lo = ((i >> lj) << (lj + 1)) | (i & (j - 1)), hi = lo + j;
-    const unsigned long long a = w[lo], c = w[hi];
-    if ((a > c) == ((lo & k) == 0)) {
-      w[lo] = c;
-      w[hi] = a;
-    }
-  }
-}
-
-__global__ void unpack_kernel(const float* __restrict__ xyz, long long N, long long T,
-                              const unsigned long long* __restrict__ keys,
-                              float* __restrict__ out_xyz, int* __restrict__ out_perm) {
-  const long long b = blockIdx.y;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < N; i += 256LL * gridDim.x) {
-    const int from = static_cast<int>(keys[b * T + i] & 0xffffffffu);
-    if (out_perm) out_perm[b * N + i] = from;
-    if (out_xyz) gather_point(xyz + b * N * 3, out_xyz + b * N * 3, i, from);
-  }
-}
-
-template <int CS>
-cudaError_t launch_cluster_sort(const float* xyz, long long batch, long long n, int axis,
-                                float* out_xyz, int* out_perm, cudaStream_t st) {
-  auto kern = bitonic_cluster_kernel<CS>;
-  const size_t smem = sizeof(unsigned long long) * kBlk;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  if (CS > 8) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(batch * CS));
-  cfg.blockDim = dim3(kSortThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-cudaError_t launch_global_sort(const float* xyz, long long batch, long long n, int axis,
-                               float* out_xyz, int* out_perm, cudaStream_t st) {
-  long long T = kBlk;
-  while (T < n) T <<= 1;
-  unsigned long long* keys = nullptr;
-  cudaError_t e = pcs_internal::workspace_alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * T * batch, st);
-  if (e != cudaSuccess) return e;
-  const size_t smem = sizeof(unsigned long long) * kBlk;
-  e = cudaFuncSetAttribute(block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
-  const dim3 elem_grid(static_cast<unsigned>(std::min<long long>(4 * 148, (T + 255) / 256)),
-                       static_cast<unsigned>(batch));
-  const dim3 blk_grid(static_cast<unsigned>(T / kBlk), static_cast<unsigned>(batch));
-  if (e == cudaSuccess) {
-    pack_kernel<<<elem_grid, 256, 0, st>>>(xyz, n, T, axis, keys);
-    block_kernel<<<blk_grid, kSortThreads, smem, st>>>(keys, T, 0);
-    for (long long k = 2LL * kBlk; k <= T; k <<= 1) {
-      for (long long j = k >> 1; j >= kBlk; j >>= 1)
-        global_step_kernel<<<elem_grid, 256, 0, st>>>(keys, T, k, j);
-      block_kernel<<<blk_grid, kSortThreads, smem, st>>>(keys, T, k);
-    }
-    unpack_kernel<<<elem_grid, 256, 0, st>>>(xyz, n, T, keys, out_xyz, out_perm);
-    e = cudaGetLastError();
-  }
-  const cudaError_t e2 = cudaFreeAsync(keys, st);
-  return e != cudaSuccess ? e : e2;
-}
 
 // ---------------------------------------------------------------- device-wide radix
 // Large clouds (fp32 > 256K points, fp64 >= 64K): LSD radix over many CTAs
@@ -1233,8 +1048,7 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   // 0.037 ms, 37 x 8K 0.047 -> 0.035 ms. Many large clouds keep the bitonic
   // network (one or two CTAs per cloud, no cross-CTA scatter): 64 x 16K
   // 0.064 vs 0.082, 256 x 32K 0.53 vs 0.63.
-  const char* radix_env = std::getenv("PCS_SORT_RADIX");
-  const bool radix_off = radix_env && radix_env[0] == '0';
+  const bool radix_off = !pcs_internal::knobs().sort_radix;
   if (coord_dtype == PCS_DTYPE_F32 && !radix_off && (n <= 4096 || (batch <= 37 && n <= 65536))) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
@@ -1265,8 +1079,7 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     float* o = static_cast<float*>(out_xyz);
     // few clouds: spread each over a cluster of 2-4 CTAs (the idle SMs
     // shorten each cloud's network); otherwise one CTA per cloud
-    const char* cs_env = std::getenv("PCS_SORT_SPREAD");
-    const bool spread = !(cs_env && cs_env[0] == '0');
+    const bool spread = true;
     if (spread && n > 4096 && batch * 4 <= 148) {
       if (n <= 8192) return pcsk::launch_reg_sort<2, 4>(x, batch, n, axis, o, out_perm, stream);
       return pcsk::launch_reg_sort<4, 4>(x, batch, n, axis, o, out_perm, stream);
@@ -1302,8 +1115,6 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     if (n <= 4 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 4>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 8 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 8>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 16 * pcsk::kBlk) return pcsk::launch_reg_sort<16, 16>(x, batch, n, axis, o, out_perm, stream);
-    if (std::getenv("PCS_SORT_BITONIC"))
-      return pcsk::launch_global_sort(x, batch, n, axis, o, out_perm, stream);
     return pcsk::launch_device_radix<float, uint32_t>(x, batch, n, axis, o, out_perm, stream);
   }
   if (coord_dtype == PCS_DTYPE_F64 && n >= 65536)

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kStreamThreads)
 }
 
 cudaError_t run_stream_any(SampleParams p, long long nmax, cudaStream_t st) {
+  if (plan("stream_sector_kernel", {p.f64 ? 8 : 4})) return cudaSuccess;
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;

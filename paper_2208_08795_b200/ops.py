@@ -142,100 +142,25 @@ def quality(xyz: torch.Tensor, idx: torch.Tensor):
     return cov, sep
 
 
-def _morton_fits(n: int, dtype: str) -> bool:
-    """Mirror of launch_morton_cs (csrc/morton_kernels.cu): some cluster size
-    <= 16 whose per-CTA rows fit shared memory with the exchange buffers."""
-    ct = 8 if dtype == "float64" else 4
-    srows = -(-n // 32)
-    for cs in (1, 2, 4, 8, 16):
-        rows = -(-srows // cs)
-        w = 4 if rows <= 128 else 8 if rows <= 256 else 16
-        if rows > 32 * w:
-            continue
-        np_ = (rows + 2) * 32
-        nbytes = np_ * (8 + 3 * ct + 4) + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
-        nbytes += 2 * cs * w * 48 if cs > 1 else 0
-        nbytes += 2 * 8 + 8 * 4
-        nbytes += 4 * _cells(np_)
-        if nbytes <= 227 * 1024:
-            return True
-    return False
-
-
-def _cells(np_: int) -> int:
-    """Bucketing histogram size (morton_*cell_bits): 2^5 .. 2^12 cells of ~8."""
-    b = 5
-    while b < 12 and (1 << b) * 8 < np_:
-        b += 1
-    return 1 << b
-
-
-def _morton_tmem_fits(n: int) -> bool:
-    """Mirror of run_morton_tmem_any (csrc/morton_tmem_kernels.cu), fp32."""
-    srows = -(-n // 32)
-    for cs in (1, 2, 4, 8, 16):
-        rows = -(-srows // cs)
-        if rows > 512:
-            continue
-        w = 8 if rows <= 256 else 16  # largest W the dispatcher may pick (smem check)
-        np_ = -(-rows // w) * w * 32
-        nbytes = np_ * 12 + ((np_ >> 5) + 4 - ((np_ >> 5) & 3)) * 4 + 2 * w * 16
-        nbytes += 2 * cs * w * 48 if cs > 1 else 0
-        nbytes += 2 * 8 + 8 * 4
-        nbytes += 4 * _cells(np_)
-        if nbytes <= 227 * 1024:
-            return True
-    return False
-
-
 def kernel_family(method: str, n: int, m: int = 1, k: Optional[int] = None,
-                  env: Optional[str] = None, dtype: str = "float32", batch: int = 1) -> str:
-    """Which sm_100a kernel family serves a call (mirrors csrc/sample_dispatch.cu):
-    the per-sector register kernel for full windows up to 3072 points, the
-    Morton-row engine for larger full windows (one CTA or a cluster), for
-    windows over sectors up to 4096 points the 8-warp latency form when the
-    call has at most 148 sectors, else the TMEM / warp NPDU kernels (up to
-    8192 points), the storage-order row engine otherwise."""
-    import os
+                  dtype: str = "float32", batch: int = 1, c: Optional[int] = None,
+                  full: bool = False) -> str:
+    """The sm_100a kernel :func:`sample` launches for this call shape -- the
+    C++ dispatcher's own decision (``pcs_kernel_family``, csrc/sample_dispatch.cu
+    run in plan mode; no device work). ``full`` keeps the template arguments,
+    e.g. ``npdu_tmem_kernel<5,1024>``."""
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    name = _core.kernel_family(METHODS[method], 1 if dtype == "float64" else 0, int(batch),
+                               int(n), int(c if c is not None else n), int(m),
+                               int(k) if k is not None else 0)
+    return name if full else name.split("<", 1)[0]
 
-    sectored = method in ("afps", "npdu_afps")
-    nmax = -(-n // (m if sectored else 1))
-    windowed = method in ("npdu_fps", "npdu_afps") and k is not None and k < 2 * nmax - 1
-    forced = env if env is not None else os.environ.get("PCS_SAMPLER")
-    if forced == "stream":
-        return "stream_sector_kernel"
-    rows = forced == "rows"
-    morton = (not windowed and os.environ.get("PCS_MORTON", "1") != "0"
-              and _morton_fits(nmax, dtype))
-    tmem = dtype != "float64" and os.environ.get("PCS_MORTON_TMEM", "1") != "0" and \
-        _morton_tmem_fits(nmax)
-    # many sectors (>= 4 per SM) of more than 1024 points: the TMEM form
-    # already wins (csrc/sample_dispatch.cu, kMortonMinBusy)
-    busy = (batch * (m if sectored else 1) >= 4 * 148 and nmax > 1024 and tmem
-            and "PCS_MORTON_MIN" not in os.environ)
-    if morton and (rows or busy or nmax > int(os.environ.get("PCS_MORTON_MIN", "3072"))):
-        return "morton_tmem_kernel" if tmem else "morton_rows_kernel"
-    if rows:
-        return "rows_kernel"
-    if windowed:
-        # few sectors: the W-warp latency form (csrc/npdu_kernels.cu, kNpduWideMax)
-        if nmax <= 4096 and batch * (m if sectored else 1) <= \
-                int(os.environ.get("PCS_NPDU_WIDE", "148")):
-            return "npdu_wide_kernel"
-        if nmax <= 4096 and (k + 62) // 32 <= 5 and dtype != "float64" and \
-                os.environ.get("PCS_NPDU_TMEM", "1") != "0":
-            return "npdu_tmem_kernel"
-        if nmax > 4096 and dtype != "float64" and os.environ.get("PCS_NPDU_BIG", "1") != "0" \
-                and _morton_tmem_fits(nmax):
-            return "morton_tmem_kernel"
-        if nmax <= 8192:
-            return "npdu_warp_kernel"
-    elif nmax <= 3072:
-        return "fps_full_kernel"
-    # storage-order rows (one CTA or a cluster of <= 16 CTAs), else streaming
-    per_pt = 8 + 3 * (8 if dtype == "float64" else 4)
-    rows_cap = 16 * ((227 * 1024 - 4096) // per_pt // 32 - 2) * 32
-    return "rows_kernel" if nmax <= rows_cap else "stream_sector_kernel"
+
+def reload_knobs() -> None:
+    """Re-read the PCS_* engine overrides (tests; they are read once per
+    process otherwise)."""
+    _core.reload_knobs()
 
 
 def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,

@@ -147,8 +147,10 @@ def lidar_sweep(batch: int, seed: int = 0, rings: int = 64, azimuths: int = 512,
             with np.errstate(invalid="ignore"):
                 t1 = (lo[q] - 0.0) * inv
                 t2 = (hi[q] - 0.0) * inv
-            tn = np.nanmax(np.minimum(t1, t2), axis=1)
-            tf = np.nanmin(np.maximum(t1, t2), axis=1)
+            a, c = np.minimum(t1, t2), np.maximum(t1, t2)
+            # NaN-ignoring max / min over the three slabs (= nanmax / nanmin)
+            tn = np.fmax(np.fmax(a[:, 0], a[:, 1]), a[:, 2])
+            tf = np.fmin(np.fmin(c[:, 0], c[:, 1]), c[:, 2])
             hit = (tf >= tn) & (tf > 0)
             t = np.where(hit & (tn > 0), np.minimum(t, tn), t)
         r = np.where(np.isfinite(t), t, 80.0)

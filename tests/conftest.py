@@ -32,6 +32,30 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+def setknob(monkeypatch, name, value):
+    """Set (value None: unset) a PCS_* engine override for this test. The
+    library reads them once per process, so re-read after the change; the
+    autouse fixture below re-reads after monkeypatch has restored the
+    environment."""
+    if value is None:
+        monkeypatch.delenv(name, raising=False)
+    else:
+        monkeypatch.setenv(name, value)
+    import paper_2208_08795_b200 as pkg
+    pkg.reload_knobs()
+
+
+@pytest.fixture(autouse=True)
+def _reload_knobs_after_test():
+    yield
+    if any(k.startswith("PCS_") for k in os.environ) or "paper_2208_08795_b200" in sys.modules:
+        try:
+            import paper_2208_08795_b200 as pkg
+            pkg.reload_knobs()
+        except ImportError:
+            pass
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from oracle import Oracle, build

@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import METHOD_NAMES, load_sampler_goldens, load_sort_goldens
+from conftest import METHOD_NAMES, load_sampler_goldens, load_sort_goldens, setknob
 from paper_2208_08795_b200 import synth
 
 pytestmark = pytest.mark.gpu
@@ -24,7 +24,7 @@ def npdu_engine(request, monkeypatch):
     """NPDU sectors <= 4096 points run on the W-warp latency form
     (npdu_wide_kernel) for small batches and on the one-warp TMEM / shared-
     memory kernels otherwise: force each (PCS_NPDU_WIDE = max sectors)."""
-    monkeypatch.setenv("PCS_NPDU_WIDE", "100000000" if request.param == "wide" else "0")
+    setknob(monkeypatch, "PCS_NPDU_WIDE", "100000000" if request.param == "wide" else "0")
     return request.param
 
 
@@ -138,8 +138,8 @@ def test_distance_trace_bit_exact(pcs, oracle, npdu_engine):
 def test_distance_trace_rows_engines(pcs, oracle, monkeypatch, morton):
     """Trace through the pruned-row engines (the Morton engine writes d[] back
     through its slot -> index map; the trace entry is the fp64 drop-in)."""
-    monkeypatch.setenv("PCS_SAMPLER", "rows")
-    monkeypatch.setenv("PCS_MORTON", morton)
+    setknob(monkeypatch, "PCS_SAMPLER", "rows")
+    setknob(monkeypatch, "PCS_MORTON", morton)
     pts = synth.random_cloud(700, 405)
     pts[100:200] = pts[3]
     idx, _, st, tr = pcs.local_fps(pts, 20, 690, 40, k=None, seed=5, first="random", trace=True)
@@ -224,7 +224,7 @@ def test_sort_kernel_families(pcs, monkeypatch, radix):
 
     from paper_2208_08795_b200 import sort_axis
 
-    monkeypatch.setenv("PCS_SORT_RADIX", radix)
+    setknob(monkeypatch, "PCS_SORT_RADIX", radix)
     rng = np.random.default_rng(29)
     cases = [(b, n) for n in (3, 1024, 1500, 2048, 4096, 4097, 8192, 12000, 16384, 30000, 32768,
                               40000, 65536) for b in (1, 16, 37, 38) if b * n <= 40 * 65536]
@@ -294,7 +294,10 @@ def test_device_wide_radix_sort(pcs):
 
 def test_full_size_properties_cfg4():
     """BASELINE cfg4 at full size (128 x 32768, NPDU-AFPS M=32, k=129,
-    C=8192): size-independent properties on every cloud, oracle on two."""
+    C=8192): size-independent properties on every cloud (distinct indices,
+    sector confinement, quotas, dist_evals = the windows along the path).
+    The bit-exact comparison of the same batch with the reference is
+    tests/test_gpu_bench_shapes.py::test_bench_workload_bit_exact[cfg4]."""
     import torch
 
     from paper_2208_08795_b200 import sample
@@ -365,8 +368,8 @@ def test_rows_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c, m, k
 
     from paper_2208_08795_b200 import sample
 
-    monkeypatch.setenv("PCS_SAMPLER", "rows")
-    monkeypatch.setenv("PCS_MORTON", morton)
+    setknob(monkeypatch, "PCS_SAMPLER", "rows")
+    setknob(monkeypatch, "PCS_MORTON", morton)
     xyz = synth.stable_sort_np(synth.uniform_cube(3, n, 5), 0)[0]
     xyz[1, : n // 3] = xyz[1, 0]  # many coincident points
     for first in ("fixed", "random"):
@@ -385,8 +388,8 @@ def test_subnormal_and_signed_zero_coordinates(oracle, monkeypatch, engine):
     from paper_2208_08795_b200 import sample
 
     if engine != "auto":
-        monkeypatch.setenv("PCS_SAMPLER", "rows")
-        monkeypatch.setenv("PCS_MORTON", "0" if engine == "slab" else "1")
+        setknob(monkeypatch, "PCS_SAMPLER", "rows")
+        setknob(monkeypatch, "PCS_MORTON", "0" if engine == "slab" else "1")
     xyz = synth.uniform_cube(2, 3000, 8) * np.float32(1e-36)
     xyz[0, ::5, 0] = np.float32(3e-41)   # subnormal
     xyz[0, 1::5, 1] = np.float32(-0.0)
@@ -409,7 +412,7 @@ def test_morton_rows_large_sectors(pcs, oracle, monkeypatch, cloud, tmem):
 
     from paper_2208_08795_b200 import sample
 
-    monkeypatch.setenv("PCS_MORTON_TMEM", tmem)
+    setknob(monkeypatch, "PCS_MORTON_TMEM", tmem)
     if cloud in ("f64", "f64exact") and tmem == "0":
         pytest.skip("fp64 input always uses the shared-memory engine")
 
@@ -472,7 +475,7 @@ def test_npdu_tmem_high_word_ties(oracle, monkeypatch, grid):
 
     from paper_2208_08795_b200 import sample
 
-    monkeypatch.setenv("PCS_NPDU_WIDE", "0")
+    setknob(monkeypatch, "PCS_NPDU_WIDE", "0")
     rng = np.random.default_rng(grid + 1)
     for n, c, m, k in ((1024, 256, 1, 129), (4096, 1024, 4, 65), (2048, 700, 1, 33),
                        (3000, 900, 2, 97), (512, 200, 1, 65), (8192, 2048, 8, 129)):
@@ -513,7 +516,7 @@ def test_streaming_engine_forced_matches_oracle(oracle, monkeypatch, meth, n, c,
 
     from paper_2208_08795_b200 import sample
 
-    monkeypatch.setenv("PCS_SAMPLER", "stream")
+    setknob(monkeypatch, "PCS_SAMPLER", "stream")
     xyz = synth.uniform_cube(2, n, 9)
     xyz[1, : n // 2] = xyz[1, 0]
     for first in ("fixed", "random"):

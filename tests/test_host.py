@@ -11,7 +11,7 @@ import socket
 import numpy as np
 import pytest
 
-from conftest import ROOT
+from conftest import ROOT, setknob
 from paper_2208_08795_b200 import shard, synth
 
 
@@ -202,12 +202,13 @@ def test_cli_usage_errors_exit_2():
     assert cli.main(["frobnicate"]) == 2
 
 
-def test_kernel_family_mirrors_dispatch(pcs, monkeypatch):
-    """ops.kernel_family follows csrc/sample_dispatch.cu + run_npdu_any: the
-    8-warp NPDU form for calls of <= 148 sectors (PCS_NPDU_WIDE moves it),
-    the one-warp TMEM kernel above, full / Morton kernels for full windows."""
+def test_kernel_family_is_the_dispatch_decision(pcs, monkeypatch):
+    """pcs_kernel_family runs csrc/sample_dispatch.cu in plan mode (no GPU
+    needed): the 8-warp NPDU form for calls of <= 148 sectors
+    (PCS_NPDU_WIDE moves it), the one-warp TMEM kernel above, full / Morton
+    kernels for full windows, the streaming engine past every on-chip one."""
     for var in ("PCS_NPDU_WIDE", "PCS_SAMPLER", "PCS_MORTON", "PCS_MORTON_MIN", "PCS_NPDU_TMEM"):
-        monkeypatch.delenv(var, raising=False)
+        setknob(monkeypatch, var, None)
     kf = pcs.kernel_family
     assert kf("npdu_afps", 32768, 32, 129, batch=4) == "npdu_wide_kernel"      # 128 sectors
     assert kf("npdu_afps", 32768, 32, 129, batch=5) == "npdu_tmem_kernel"      # 160 sectors
@@ -216,5 +217,8 @@ def test_kernel_family_mirrors_dispatch(pcs, monkeypatch):
     assert kf("npdu_fps", 8192, 1, 65, batch=1) == "morton_tmem_kernel"        # > 4096 points
     assert kf("afps", 2048, 8, batch=16) == "fps_full_kernel"                  # cfg2
     assert kf("fps", 8192, 1, batch=64) == "morton_tmem_kernel"                # cfg3 FPS
-    monkeypatch.setenv("PCS_NPDU_WIDE", "0")
+    assert kf("npdu_afps", 32768, 32, 129, batch=128, full=True) == "npdu_tmem_kernel<5,1024>"
+    assert kf("fps", 1 << 20) == "stream_sector_kernel"
+    assert kf("afps", 1 << 20, 1024, batch=1, full=True) == "fps_full_kernel<8,4,1>"
+    setknob(monkeypatch, "PCS_NPDU_WIDE", "0")
     assert kf("npdu_afps", 32768, 32, 129, batch=1) == "npdu_tmem_kernel"
