@@ -357,8 +357,9 @@ class Runner:
         w, pcs, sh = self.w, self.pcs, self.sh
         if sh is None:
             return pcs.sample(xs, w["C"], method=w["method"], m=w["M"], k=w["K"])
-        return pcs.sample(xs[:, sh.point_lo:sh.point_hi], sh.c, method=w["method"], m=sh.m,
-                          k=w["K"], index_base=sh.point_lo, sector_base=sh.sector_lo)
+        from paper_2208_08795_b200 import shard
+
+        return shard.sample_sector_shard(xs, sh, w["method"], w["K"])
 
     def step(self, x):
         w, pcs = self.w, self.pcs
@@ -626,8 +627,9 @@ def main():
     flops = 8.0 * evals_local
     achieved = flops / (kern_ms * 1e-3) / 1e12
     traffic, traffic_src, ipc, fp64_pct = ncu_traffic(args.workload)
-    kernel = pcs.kernel_family(w["method"], sh.n if sh else N, sh.m if sh else w["M"], w["K"],
-                               batch=xyz_host.shape[0])
+    kernel = ("none (empty shard)" if sh is not None and sh.empty else
+              pcs.kernel_family(w["method"], sh.n if sh else N, sh.m if sh else w["M"], w["K"],
+                                batch=xyz_host.shape[0]))
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if peak else None,
                 "traffic": traffic if world == 1 and mode == "batch" else None,

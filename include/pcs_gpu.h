@@ -27,6 +27,9 @@
  *   pcs_gpu_sort_axis    <- batched device form of exact_sort
  *   pcs_sample_host_batch <- the per-cloud samplers called over a batch of
  *                           host clouds (+ exact_sort), in one pipelined call
+ *   pcs_sample_host_multi <- the same batch spread over several devices: the
+ *                           cross-GPU form of the reference's sector work
+ *                           split + ordered merge, src/sampler.cpp:25-79
  *
  * Semantics are the reference's, bit for bit: indices, sector_of and the
  * OpStats counters (include/pcs/op_stats.hpp:10-25) equal the reference CPU
@@ -134,6 +137,22 @@ int pcs_sample_host(int32_t method, const double* xyz, int64_t n, int64_t c, int
  * Synchronous. */
 int pcs_sample_host_batch(const pcs_gpu_args* host_args, int32_t sort_axis, int32_t* out_perm,
                           int32_t chunks);
+
+/* Multi-device host batch (one process, several GPUs): as
+ * pcs_sample_host_batch, with the work split over `devices[0..ndevices)`
+ * (CUDA ordinals; repeats allowed -- shards on one device run in turn).
+ * Clouds split by cloud, device r taking the r-th of ndevices contiguous
+ * runs (the first B % ndevices one cloud larger, partition_sectors' rule,
+ * src/sectors.cpp:9-24). A single cloud under AFPS / NPDU-AFPS with
+ * m >= ndevices splits by sector run instead: every device copies and sorts
+ * the whole cloud, samples its sectors with the global index / sector bases
+ * (so indices, sector_of and the seed ^ sector starts are the one-device
+ * ones), and its indices fill its slots of the row; stats are summed.
+ * Results are written straight into the host outputs -- the only "gather".
+ * No collective and no peer traffic. Synchronous; bit-identical to
+ * pcs_sample_host_batch on one device. */
+int pcs_sample_host_multi(const pcs_gpu_args* host_args, int32_t sort_axis, int32_t* out_perm,
+                          const int32_t* devices, int32_t ndevices);
 
 /* detail::local_fps over one storage range [sector_begin, sector_end) of a
  * cloud. k < 0 means no window (std::nullopt); k == 0 is rejected exactly as

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -271,18 +272,22 @@ cudaError_t device_streams(DevStreams** out) {
 
 }  // namespace
 
-int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
-                          int32_t chunks) {
-  clear_error();
-  if (!ha) { set_error("pcs_sample_host_batch: null args"); return PCS_ERR_INVALID_ARGUMENT; }
+namespace {
+
+int fail_to(cudaError_t e, const std::string& extra, std::string* err) {
+  const int rc = cuda_fail(e, extra);
+  *err = pcs_last_error();
+  return rc;
+}
+
+// The host-batch pipeline on the calling thread's current device (arguments
+// already validated). Thread-safe: callers on one device serialise on its
+// stream set. Errors go to *err (the caller may be a worker thread).
+int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
+                      int32_t chunks, std::string* err) {
   std::string msg;
-  int rc = validate_sample(ha->method, ha->n, ha->c, ha->m, ha->k, &msg);
-  if (rc) { set_error(msg); return rc; }
-  if (ha->batch < 0) { set_error("pcs_sample_host_batch: batch must be >= 0"); return PCS_ERR_INVALID_ARGUMENT; }
-  if (sort_axis < -1 || sort_axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
   const int64_t B = ha->batch, N = ha->n, C = ha->c;
   if (B == 0) return PCS_OK;
-  if (!ha->xyz || !ha->out_indices) { set_error("pcs_sample_host_batch: null buffer"); return PCS_ERR_INVALID_ARGUMENT; }
   const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
   const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
   const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
@@ -302,7 +307,7 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
   int nch = static_cast<int>(bounds.size()) - 1;
   DevStreams* dsp = nullptr;
   cudaError_t e = device_streams(&dsp);
-  if (e != cudaSuccess) return cuda_fail(e);
+  if (e != cudaSuccess) return fail_to(e, "", err);
   std::lock_guard<std::mutex> lock(dsp->mu);
   DevStreams& ds = *dsp;
   cudaStream_t copy = ds.copy;
@@ -374,7 +379,183 @@ int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* ou
     const cudaError_t e2 = cudaStreamSynchronize(copy);
     if (e == cudaSuccess) e = e2;
   }
-  if (e != cudaSuccess) return cuda_fail(e, msg);
+  if (e != cudaSuccess) return fail_to(e, msg, err);
+  return PCS_OK;
+}
+
+
+// One storage slice (a run of sectors) of a single cloud on the current
+// device: the whole cloud goes over and is sorted there (every device sorts
+// it itself -- the sort is cheap next to a cross-device broadcast), then the
+// slice [point_lo, point_hi) is sampled with the global index / sector
+// bases; its indices land in out slots [out_lo, out_lo + c) of the row.
+int host_sector_slice(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
+                      int64_t point_lo, int64_t point_hi, int64_t sector_lo, int64_t m,
+                      int64_t out_lo, int64_t c, uint64_t* stats, std::string* err) {
+  std::string msg;
+  const int64_t N = ha->n;
+  const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
+  const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
+  const size_t cloud_bytes = csize * 3 * static_cast<size_t>(N);
+  DevStreams* dsp = nullptr;
+  cudaError_t e = device_streams(&dsp);
+  if (e != cudaSuccess) return fail_to(e, "", err);
+  std::lock_guard<std::mutex> lock(dsp->mu);
+  cudaStream_t st = dsp->work[0];
+  size_t bytes = 0, off_srt = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
+  auto take = [&](size_t& off, size_t len) { off = bytes; bytes += (len + 255) & ~size_t(255); };
+  size_t off_xyz = 0;
+  take(off_xyz, cloud_bytes);
+  take(off_srt, sort_axis >= 0 ? cloud_bytes : 0);
+  take(off_perm, sort_axis >= 0 ? 4 * static_cast<size_t>(N) : 0);
+  take(off_idx, isize * static_cast<size_t>(c));
+  take(off_sec, 4 * static_cast<size_t>(c));
+  take(off_st, 32);
+  take(off_seed, 8);
+  void* ws = nullptr;
+  e = workspace_alloc(&ws, bytes, st);
+  if (e != cudaSuccess) return fail_to(e, "", err);
+  char* base = static_cast<char*>(ws);
+  e = cudaMemcpyAsync(base + off_xyz, ha->xyz, cloud_bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && ha->seeds)
+    e = cudaMemcpyAsync(base + off_seed, ha->seeds, 8, cudaMemcpyHostToDevice, st);
+  const char* src = base + off_xyz;
+  int32_t* dperm = reinterpret_cast<int32_t*>(base + off_perm);
+  if (e == cudaSuccess && sort_axis >= 0) {
+    e = launch_sort(ha->coord_dtype, base + off_xyz, 1, N, sort_axis, base + off_srt, dperm, st);
+    src = base + off_srt;
+  }
+  pcs_gpu_args a = *ha;
+  a.xyz = src + csize * 3 * static_cast<size_t>(point_lo);
+  a.batch = 1;
+  a.n = point_hi - point_lo;
+  a.m = m;
+  a.c = c;
+  a.index_base = ha->index_base + point_lo;
+  a.sector_base = ha->sector_base + sector_lo;
+  a.seeds = ha->seeds ? reinterpret_cast<const uint64_t*>(base + off_seed) : nullptr;
+  a.out_indices = base + off_idx;
+  a.out_sector = reinterpret_cast<int32_t*>(base + off_sec);
+  a.out_stats = reinterpret_cast<uint64_t*>(base + off_st);
+  if (e == cudaSuccess) e = launch_sample(a, st, &msg);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(static_cast<char*>(ha->out_indices) + isize * out_lo, a.out_indices,
+                        isize * c, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && ha->out_sector)
+    e = cudaMemcpyAsync(ha->out_sector + out_lo, a.out_sector, 4 * c, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(stats, a.out_stats, 32, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && sort_axis >= 0 && out_perm)
+    e = cudaMemcpyAsync(out_perm, dperm, 4 * N, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(ws, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = e2;
+  return e == cudaSuccess ? PCS_OK : fail_to(e, msg, err);
+}
+
+int check_host_args(const pcs_gpu_args* ha, int32_t sort_axis, const char* who) {
+  if (!ha) { set_error(std::string(who) + ": null args"); return PCS_ERR_INVALID_ARGUMENT; }
+  std::string msg;
+  const int rc = validate_sample(ha->method, ha->n, ha->c, ha->m, ha->k, &msg);
+  if (rc) { set_error(msg); return rc; }
+  if (ha->batch < 0) { set_error(std::string(who) + ": batch must be >= 0"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (sort_axis < -1 || sort_axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (ha->batch > 0 && (!ha->xyz || !ha->out_indices)) { set_error(std::string(who) + ": null buffer"); return PCS_ERR_INVALID_ARGUMENT; }
+  return PCS_OK;
+}
+
+// [lo, hi) of part r of `total` split `parts` ways, the first total % parts
+// parts one larger (partition_sectors' rule, proj/src/sectors.cpp:9-24)
+void split_range(int64_t total, int64_t parts, int64_t r, int64_t* lo, int64_t* hi) {
+  const int64_t base = total / parts, rem = total % parts;
+  *lo = r * base + std::min(r, rem);
+  *hi = *lo + base + (r < rem ? 1 : 0);
+}
+
+}  // namespace
+
+int pcs_sample_host_batch(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
+                          int32_t chunks) {
+  clear_error();
+  int rc = check_host_args(ha, sort_axis, "pcs_sample_host_batch");
+  if (rc) return rc;
+  std::string err;
+  rc = host_batch_device(ha, sort_axis, out_perm, chunks, &err);
+  if (rc) set_error(err);
+  return rc;
+}
+
+int pcs_sample_host_multi(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_perm,
+                          const int32_t* devices, int32_t ndevices) {
+  clear_error();
+  int rc = check_host_args(ha, sort_axis, "pcs_sample_host_multi");
+  if (rc) return rc;
+  if (!devices || ndevices < 1) { set_error("pcs_sample_host_multi: need at least one device"); return PCS_ERR_INVALID_ARGUMENT; }
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int i = 0; i < ndevices; ++i)
+    if (devices[i] < 0 || devices[i] >= count) { set_error("pcs_sample_host_multi: no such device " + std::to_string(devices[i])); return PCS_ERR_INVALID_ARGUMENT; }
+  const int64_t B = ha->batch;
+  if (B == 0) return PCS_OK;
+  const bool sectored = ha->method == PCS_METHOD_AFPS || ha->method == PCS_METHOD_NPDU_AFPS;
+  const bool by_sector = B == 1 && sectored && ndevices > 1 && ha->m >= ndevices;
+  const int64_t parts = by_sector ? ndevices : std::min<int64_t>(ndevices, B);
+  std::vector<int> rcs(parts, PCS_OK);
+  std::vector<std::string> errs(parts);
+  std::vector<uint64_t> stats(4 * parts, 0);
+  const size_t csize = ha->coord_dtype == PCS_DTYPE_F64 ? 8 : 4;
+  const size_t isize = ha->index_dtype == PCS_INDEX_I64 ? 8 : 4;
+  auto work = [&](int64_t r) {
+    cudaError_t ce = cudaSetDevice(devices[r]);
+    if (ce != cudaSuccess) { rcs[r] = fail_to(ce, "", &errs[r]); return; }
+    if (by_sector) {
+      // one cloud: a contiguous run of sectors per device; with the
+      // reference's remainder rule a run re-partitions to the same
+      // boundaries and quotas (sectors.cpp:9-36)
+      int64_t s0, s1, p0, p1, o0, o1, t;
+      split_range(ha->m, parts, r, &s0, &s1);
+      split_range(ha->n, ha->m, s0, &p0, &t);
+      split_range(ha->n, ha->m, s1, &p1, &t);
+      split_range(ha->c, ha->m, s0, &o0, &t);
+      split_range(ha->c, ha->m, s1, &o1, &t);
+      if (s1 == ha->m) { p1 = ha->n; o1 = ha->c; }
+      rcs[r] = host_sector_slice(ha, sort_axis, r == 0 ? out_perm : nullptr, p0, p1, s0,
+                                 s1 - s0, o0, o1 - o0, &stats[4 * r], &errs[r]);
+      return;
+    }
+    int64_t b0, b1;
+    split_range(B, parts, r, &b0, &b1);
+    pcs_gpu_args a = *ha;
+    a.batch = b1 - b0;
+    a.xyz = static_cast<const char*>(ha->xyz) + csize * 3 * static_cast<size_t>(ha->n) * b0;
+    a.seeds = ha->seeds ? ha->seeds + b0 : nullptr;
+    a.out_indices = static_cast<char*>(ha->out_indices) + isize * static_cast<size_t>(ha->c) * b0;
+    a.out_sector = ha->out_sector ? ha->out_sector + ha->c * b0 : nullptr;
+    a.out_stats = ha->out_stats ? ha->out_stats + 4 * b0 : nullptr;
+    rcs[r] = host_batch_device(&a, sort_axis, out_perm ? out_perm + ha->n * b0 : nullptr, 0,
+                               &errs[r]);
+  };
+  int prev = 0;
+  e = cudaGetDevice(&prev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  {
+    std::vector<std::thread> pool;
+    for (int64_t r = 1; r < parts; ++r) pool.emplace_back(work, r);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  cudaSetDevice(prev);
+  for (int64_t r = 0; r < parts; ++r)
+    if (rcs[r] != PCS_OK) {
+      set_error(errs[r]);
+      return rcs[r];
+    }
+  if (by_sector && ha->out_stats)
+    for (int j = 0; j < 4; ++j) {
+      uint64_t sum = 0;
+      for (int64_t r = 0; r < parts; ++r) sum += stats[4 * r + j];
+      ha->out_stats[j] = sum;
+    }
   return PCS_OK;
 }
 

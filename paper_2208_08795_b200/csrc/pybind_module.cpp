@@ -318,7 +318,7 @@ PYBIND11_MODULE(_core, m) {
            std::int64_t c, std::int64_t mm, std::int64_t k, int seed_policy, std::uint64_t seed,
            std::uintptr_t seeds, int index_dtype, std::uintptr_t out_idx, std::uintptr_t out_sector,
            std::uintptr_t out_stats, int sort_axis, std::uintptr_t out_perm, int chunks,
-           std::int64_t index_base, std::int64_t sector_base) {
+           std::int64_t index_base, std::int64_t sector_base, std::vector<int> devices) {
           pcs_gpu_args a{};
           a.index_base = index_base;
           a.sector_base = sector_base;
@@ -340,8 +340,12 @@ PYBIND11_MODULE(_core, m) {
           int rc;
           {
             py::gil_scoped_release nogil;
-            rc = pcs_sample_host_batch(&a, sort_axis, reinterpret_cast<std::int32_t*>(out_perm),
-                                       chunks);
+            if (devices.empty())
+              rc = pcs_sample_host_batch(&a, sort_axis, reinterpret_cast<std::int32_t*>(out_perm),
+                                         chunks);
+            else
+              rc = pcs_sample_host_multi(&a, sort_axis, reinterpret_cast<std::int32_t*>(out_perm),
+                                         devices.data(), static_cast<std::int32_t>(devices.size()));
           }
           check(rc);
         },
@@ -349,7 +353,8 @@ PYBIND11_MODULE(_core, m) {
         py::arg("c"), py::arg("m"), py::arg("k"), py::arg("seed_policy"), py::arg("seed"),
         py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
         py::arg("out_stats"), py::arg("sort_axis"), py::arg("out_perm"), py::arg("chunks") = 0,
-        py::arg("index_base") = 0, py::arg("sector_base") = 0);
+        py::arg("index_base") = 0, py::arg("sector_base") = 0,
+        py::arg("devices") = std::vector<int>{});
   m.def("sort_device",
         [](int coord_dtype, std::uintptr_t xyz, std::int64_t batch, std::int64_t n, int axis,
            std::uintptr_t out_xyz, std::uintptr_t out_perm, std::uintptr_t stream) {

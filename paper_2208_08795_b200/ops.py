@@ -167,14 +167,20 @@ def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
                       k: Optional[int] = None, first: str = "fixed", seed: int = 0,
                       sort: Optional[str] = None, device: Optional[str] = None,
                       index_dtype=np.int32, return_sector: bool = False, chunks: int = 0,
-                      seeds=None, index_base: int = 0, sector_base: int = 0):
+                      seeds=None, index_base: int = 0, sector_base: int = 0,
+                      devices=None):
     """Host batch in, host results out, through the C-ABI host entry
     ``pcs_sample_host_batch`` (include/pcs_gpu.h): the per-cloud samplers
     over a batch in one native, pipelined call (H2D of a chunk overlaps the
     sort + sampling of the previous one). ``xyz``: (B, N, 3) float32/float64
     numpy array or CPU torch tensor (pin it -- ``tensor.pin_memory()`` -- for
     copy/compute overlap). Returns numpy ``(indices (B, c), stats (B, 4))``
-    plus ``sector_of`` when ``return_sector`` and ``perm`` when ``sort``."""
+    plus ``sector_of`` when ``return_sector`` and ``perm`` when ``sort``.
+
+    ``devices`` (a list of CUDA ordinals, e.g. ``range(8)``) spreads the
+    call over several GPUs from this one process (``pcs_sample_host_multi``):
+    clouds split by cloud, or one AFPS / NPDU-AFPS cloud by sector run;
+    results identical to the one-device call."""
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r}")
     if first not in ("fixed", "random"):
@@ -202,6 +208,7 @@ def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
         if sd.numel() != B:
             raise ValueError("seeds must hold one seed per cloud")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    devs = [int(d.index if isinstance(d, torch.device) else d) for d in devices] if devices else []
     with torch.cuda.device(dev):
         _core.sample_host_ptr(METHODS[method], 1 if x.dtype == torch.float64 else 0,
                               x.data_ptr(), B, N, int(c), int(m), int(k) if k is not None else 0,
@@ -211,7 +218,7 @@ def sample_host_batch(xyz, c: int, method: str = "afps", m: int = 1,
                               sec.data_ptr() if sec is not None else 0, stats.data_ptr(),
                               _AXES[sort] if sort is not None else -1,
                               perm.data_ptr() if perm is not None else 0, int(chunks),
-                              int(index_base), int(sector_base))
+                              int(index_base), int(sector_base), devs)
     out = [idx.numpy(), stats.numpy()]
     if return_sector:
         out.append(sec.numpy())

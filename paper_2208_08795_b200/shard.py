@@ -52,6 +52,11 @@ class SectorShard:
     def c(self):
         return self.out_hi - self.out_lo
 
+    @property
+    def empty(self):
+        """More ranks than sectors: this rank has no sector to sample."""
+        return self.m == 0
+
 
 def _start(total: int, parts: int, s: int) -> int:
     base, rem = divmod(total, parts)
@@ -62,6 +67,26 @@ def sector_shard(n: int, c: int, m: int, world: int, rank: int) -> SectorShard:
     s0, s1 = split(m, world, rank)
     return SectorShard(s0, s1, _start(n, m, s0), _start(n, m, s1), _start(c, m, s0),
                        _start(c, m, s1))
+
+
+def sample_sector_shard(sorted_xyz: torch.Tensor, sh: SectorShard, method: str, k=None,
+                        first: str = "fixed", seed: int = 0):
+    """Sample rank's run of sectors of the (already sorted) cloud(s)
+    ``sorted_xyz`` (B, N, 3) on the device: global indices, sector ids and
+    per-sector seeds. An empty shard (world > m) yields (B, 0) results, so
+    it still takes part in ``gather_rows``. Returns (indices int32,
+    stats int64 (B, 4), sector_of int32)."""
+    from . import sample
+
+    B = sorted_xyz.shape[0]
+    if sh.empty:
+        dev = sorted_xyz.device
+        return (torch.zeros((B, 0), dtype=torch.int32, device=dev),
+                torch.zeros((B, 4), dtype=torch.int64, device=dev),
+                torch.zeros((B, 0), dtype=torch.int32, device=dev))
+    return sample(sorted_xyz[:, sh.point_lo:sh.point_hi], sh.c, method=method, m=sh.m, k=k,
+                  first=first, seed=seed, return_sector=True, index_base=sh.point_lo,
+                  sector_base=sh.sector_lo)
 
 
 def gather_rows(local: torch.Tensor, total_rows: int, world: int, group=None) -> torch.Tensor | None:

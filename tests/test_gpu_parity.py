@@ -821,3 +821,140 @@ def test_cpp_dropin_api_kats():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-2000:]
     assert "all checks passed" in p.stdout
+
+
+# ---------------------------------------------------------------- §8(e) multi-GPU
+def test_host_multi_device_batch_split():
+    """pcs_sample_host_multi, batch split by cloud: several shards on this
+    box's one GPU (repeated ordinals run in turn on its stream set) give the
+    one-device results -- indices, sector_of, stats, permutation."""
+    from paper_2208_08795_b200 import sample_host_batch
+
+    xyz = synth.primitives(13, 4096, 5, seed=6)
+    one = sample_host_batch(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x",
+                            return_sector=True, first="random", seed=11,
+                            seeds=np.arange(13) * 7 + 1)
+    for devices in ([0], [0, 0], [0, 0, 0], [0] * 13, [0] * 20):
+        got = sample_host_batch(xyz, 1024, method="npdu_afps", m=8, k=65, sort="x",
+                                return_sector=True, first="random", seed=11,
+                                seeds=np.arange(13) * 7 + 1, devices=devices)
+        for a, b in zip(one, got):
+            np.testing.assert_array_equal(a, b, err_msg=str(devices))
+
+
+@pytest.mark.parametrize("meth,n,c,m,k", [("afps", 1 << 20, 1 << 18, 1024, None),
+                                          ("npdu_afps", 100003, 9001, 37, 33)])
+def test_host_multi_device_sector_split(oracle, meth, n, c, m, k):
+    """pcs_sample_host_multi on ONE large cloud: sector runs per device
+    (BASELINE cfg5's 1M-point cloud, M=1024), every device sorting the cloud
+    itself; equal to the one-device call and to the oracle."""
+    from paper_2208_08795_b200 import sample_host_batch
+
+    xyz = synth.uniform_cube(1, n, 23)
+    one = sample_host_batch(xyz, c, method=meth, m=m, k=k, sort="x", return_sector=True,
+                            first="random", seed=5)
+    for devices in ([0, 0], [0, 0, 0], [0] * 8):
+        got = sample_host_batch(xyz, c, method=meth, m=m, k=k, sort="x", return_sector=True,
+                                first="random", seed=5, devices=devices)
+        for a, b in zip(one, got):
+            np.testing.assert_array_equal(a, b, err_msg=str(devices))
+    srt = synth.stable_sort_np(xyz, 0)[0]
+    idx, sec, st = oracle.sample(meth, srt[0].astype(np.float64), c, m, k or 0, "random", 5)
+    np.testing.assert_array_equal(one[0][0], idx)
+    np.testing.assert_array_equal(one[2][0], sec)
+    np.testing.assert_array_equal(one[1][0], st.astype(np.int64))
+
+
+def _rank_worker(rank, world, port, q):
+    """One rank of the torchrun layout, both on cuda:0: the product path
+    (sort + sample of this rank's sectors with the global bases, or of its
+    clouds), then the end-of-batch gather over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_08795_b200 import sample, shard, sort_axis
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    n, c, m, k = 65536, 8192, 64, 65
+    xyz = torch.from_numpy(synth.uniform_cube(1, n, 31)).cuda()
+    srt = sort_axis(xyz, "x")[0]
+    sh = shard.sector_shard(n, c, m, world, rank)
+    idx, st, sec = shard.sample_sector_shard(srt, sh, "npdu_afps", k, first="random", seed=3)
+    rows = shard.gather_rows(torch.stack([idx[0], sec[0]], 1).cpu(), c, world)
+    stats = st[0].cpu()
+    dist.all_reduce(stats)
+    clouds = synth.primitives(6, 2048, 4, seed=2)
+    b0, b1 = shard.split(6, world, rank)
+    bi = sample(torch.from_numpy(clouds[b0:b1]).cuda(), 512, method="afps", m=8)[0].cpu()
+    brows = shard.gather_rows(bi, 6, world)
+    if rank == 0:
+        q.put((rows.numpy(), stats.numpy(), brows.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_on_the_product_path_equal_one_call(world):
+    """The multi-GPU layout of bench.py / shard.py with `world` ranks (all on
+    this box's cuda:0, gloo for the one end-of-batch gather): sector-split
+    NPDU-AFPS of one cloud and cloud-split AFPS of a batch equal the
+    single-process call bit for bit."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2208_08795_b200 import sample
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    rows, stats, brows = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    xyz = torch.from_numpy(synth.uniform_cube(1, 65536, 31)).cuda()
+    idx, st, sec, _ = sample(xyz, 8192, method="npdu_afps", m=64, k=65, sort="x",
+                             first="random", seed=3, return_sector=True)
+    np.testing.assert_array_equal(rows[:, 0], idx[0].cpu().numpy())
+    np.testing.assert_array_equal(rows[:, 1], sec[0].cpu().numpy())
+    np.testing.assert_array_equal(stats, st[0].cpu().numpy())
+    clouds = synth.primitives(6, 2048, 4, seed=2)
+    want = sample(torch.from_numpy(clouds).cuda(), 512, method="afps", m=8)[0].cpu().numpy()
+    np.testing.assert_array_equal(brows, want)
+
+
+def test_concurrent_callers_equal_serial(pcs):
+    """The b4 contract (reentrant, schedule-independent calls,
+    proj/tests/test_sampler.cpp:245-252): 8 host threads calling the drop-in
+    samplers and the host-batch entry at once (the GIL is released around
+    the native calls) get exactly the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    clouds = [synth.random_cloud(3000 + 97 * i, 40 + i) for i in range(8)]
+    batch = synth.primitives(6, 4096, 4, seed=8)
+
+    def job(i):
+        if i % 3 == 0:
+            return pcs.npdu_afps(clouds[i], 600, 6, 33, seed=i, first="random")
+        if i % 3 == 1:
+            return pcs.afps(clouds[i], 500, 4, seed=i)
+        return pcs.sample_host_batch(batch, 1024, method="npdu_afps", m=8, k=65, sort="x")
+
+    serial = [job(i) for i in range(8)]
+    for _ in range(3):
+        with ThreadPoolExecutor(8) as ex:
+            par = list(ex.map(job, range(8)))
+        for a, b in zip(serial, par):
+            np.testing.assert_array_equal(a[0], b[0])
+            if isinstance(a[2], dict):
+                assert a[2] == b[2]
+            else:
+                np.testing.assert_array_equal(a[1], b[1])
