@@ -361,6 +361,16 @@ class Runner:
 
         return shard.sample_sector_shard(xs, sh, w["method"], w["K"])
 
+    def sample_perm(self, x, perm):
+        """The step's sampler launch alone: the unsorted clouds and the sort
+        permutation (what sample(sort=...) launches after the sort)."""
+        w, pcs = self.w, self.pcs
+        if perm is None:
+            return self.sample_sorted(x)
+        from paper_2208_08795_b200 import ops
+
+        return ops.sample_with_perm(x, perm, w["C"], method=w["method"], m=w["M"], k=w["K"])
+
     def step(self, x):
         w, pcs = self.w, self.pcs
         if self.sh is None:
@@ -378,6 +388,8 @@ class Runner:
         """Sum of CUDA-event times of `fn` over `steps` calls, L2 flushed
         before each (outside the events). Returns (ms_total, last output)."""
         torch = self.torch
+        fn()  # one untimed call: first-use allocations stay outside the events
+        torch.cuda.synchronize()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         out = None
@@ -418,12 +430,15 @@ class Runner:
             dist.barrier()
         total = 0.0
         r = None
+        per_call = []
         for i in range(steps):
             self._flush(i)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             r = call()
-            total += time.perf_counter() - t0
+            dt = time.perf_counter() - t0
+            per_call.append(dt * 1e3)
+            total += dt
         e_ms = total * 1e3
         if dist is not None:
             t = torch.tensor([e_ms], dtype=torch.float64, device=self.dev)
@@ -442,7 +457,8 @@ class Runner:
             h2d.append(es.elapsed_time(ee))
         del dst
         nbytes = pinned.numel() * pinned.element_size()
-        return {"ms_per_step": e_ms, "h2d_floor_ms": min(h2d),
+        return {"ms_per_step": e_ms, "min_ms": min(per_call), "max_ms": max(per_call),
+                "h2d_floor_ms": min(h2d),
                 "h2d_gbps": nbytes / min(h2d) / 1e6, "h2d_bytes_per_step": int(nbytes),
                 "d2h_bytes_per_step": int(sum(t.nbytes if hasattr(t, "nbytes") else
                                               t.numel() * t.element_size() for t in r)),
@@ -455,9 +471,10 @@ class Runner:
 
 
 def sort_bytes(w):
-    """Algorithmic HBM bytes of the axis sort per step: read the cloud (12N),
-    write the permutation (4N) and the gathered cloud (12N)."""
-    return 0 if not w["sort"] else w["B"] * w["N"] * 28
+    """Algorithmic HBM bytes of the step's axis sort: read the cloud (12N),
+    write the permutation (4N). (The gathered copy is never written: the
+    sampler stages through the permutation.)"""
+    return 0 if not w["sort"] else w["B"] * w["N"] * 16
 
 
 def stream_bytes(w):
@@ -470,6 +487,10 @@ def stream_bytes(w):
 def measure_workload(pcs, torch, dev, name, w, steps, warmup, xyz_host, cpu_budget_s=2.0):
     """One `workloads` entry (N=1): step / sort / sampler times, kernel,
     roofline fractions, e2e, cpu_baseline and parity."""
+    import gc
+
+    gc.collect()  # the previous workload's buffers go now, not inside a timed region
+    torch.cuda.synchronize()
     r = Runner(pcs, torch, dev, w, xyz_host)
     for _ in range(warmup):
         out = r.step(r.xyz)
@@ -480,10 +501,12 @@ def measure_workload(pcs, torch, dev, name, w, steps, warmup, xyz_host, cpu_budg
     gpu_idx = out[0].cpu().numpy()
     sort_ms = 0.0
     xs = r.xyz
+    perm = None
     if w["sort"]:
-        sort_ms = r.timed(lambda: pcs.sort_axis(r.xyz, w["sort"]), steps)[0] / steps
-        xs = pcs.sort_axis(r.xyz, w["sort"])[0]
-    samp_ms = r.timed(lambda: r.sample_sorted(xs), steps)[0] / steps
+        # the step's sort: the permutation only (the sampler stages through it)
+        sort_ms = r.timed(lambda: pcs.sort_perm(r.xyz, w["sort"]), steps)[0] / steps
+        perm = pcs.sort_perm(r.xyz, w["sort"])
+    samp_ms = r.timed(lambda: r.sample_perm(xs, perm), steps)[0] / steps
     peak, _ = fp64_peak()
     hbm, _ = hbm_peak()
     kern = pcs.kernel_family(w["method"], w["N"], w["M"], w["K"], batch=w["B"])
@@ -499,7 +522,7 @@ def measure_workload(pcs, torch, dev, name, w, steps, warmup, xyz_host, cpu_budg
     if kern.startswith("stream"):
         entry["stream_hbm_frac"] = stream_bytes(w) / (samp_ms * 1e-3) / 1e9 / hbm
         entry["stream_note"] = "d[] and xyz stay L2-resident (20 B/pt x 1M < 126 MB L2)"
-    e = r.e2e(max(2, steps // 2), 2)
+    e = r.e2e(max(6, steps), 2)
     e["value"] = w["B"] * w["C"] / (e["ms_per_step"] * 1e-3)
     e["unit"] = "sampled points/s"
     entry["e2e"] = e
@@ -621,8 +644,14 @@ def main():
         del rw
 
     # ---- sampler kernel alone (roofline): sort once, time only the sampler
-    xs = pcs.sort_axis(r.xyz, w["sort"])[0] if w["sort"] else r.xyz
-    kern_ms = r.timed(lambda: r.sample_sorted(xs), args.steps, per_step_sync=True)[0] / args.steps
+    if sh is None:
+        perm = pcs.sort_perm(r.xyz, w["sort"]) if w["sort"] else None
+        kern_ms = r.timed(lambda: r.sample_perm(r.xyz, perm), args.steps,
+                          per_step_sync=True)[0] / args.steps
+    else:
+        xs = pcs.sort_axis(r.xyz, w["sort"])[0] if w["sort"] else r.xyz
+        kern_ms = r.timed(lambda: r.sample_sorted(xs), args.steps,
+                          per_step_sync=True)[0] / args.steps
     peak, peak_src = fp64_peak()
     flops = 8.0 * evals_local
     achieved = flops / (kern_ms * 1e-3) / 1e12

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define PCS_GPU_ABI_VERSION 1
+#define PCS_GPU_ABI_VERSION 2
 
 typedef enum {
   PCS_OK = 0,
@@ -102,6 +102,12 @@ typedef struct pcs_gpu_args {
    * sector_base. Zero for an ordinary call. */
   int64_t index_base;
   int64_t sector_base;
+  /* Optional device (B, N) int32 sort permutation (sorted position ->
+   * storage index, as pcs_gpu_sort_axis returns it): sample the clouds in
+   * that order, i.e. exactly as if xyz had been replaced by the sorted copy
+   * (indices refer to sorted positions) -- without the copy. NULL: storage
+   * order. Added in ABI version 2. */
+  const int32_t* perm;
 } pcs_gpu_args;
 
 /* Stream-ordered batched sampling. `stream` is a cudaStream_t (NULL = legacy
@@ -110,9 +116,11 @@ int pcs_gpu_sample(const pcs_gpu_args* args, void* stream);
 
 /* Stable ascending sort of every cloud along `axis` (0 x, 1 y, 2 z) with the
  * reference's operator< on the coordinate (-0.0 == +0.0, ties keep storage
- * order). Writes the gathered cloud (same dtype as the input; may not alias
- * xyz) and, optionally, the permutation (int32, sorted position -> original
- * index). Stream-ordered. */
+ * order). Writes, each optionally (NULL skips it), the gathered cloud (same
+ * dtype as the input; may not alias xyz) and the permutation (int32, sorted
+ * position -> original index). The permutation alone plus
+ * pcs_gpu_args.perm is the cheap way to sample sorted clouds.
+ * Stream-ordered. */
 int pcs_gpu_sort_axis(int32_t coord_dtype, const void* xyz, int64_t batch, int64_t n,
                       int32_t axis, void* out_xyz, int32_t* out_perm, void* stream);
 

@@ -30,13 +30,13 @@ except ImportError as exc:  # pragma: no cover - exercised only when unbuilt
 from ._core import (afps, coverage_radius, exact_sort, fps, local_fps, npdu_afps,  # noqa: E402
                     npdu_fps, read_cloud, separation, write_cloud)
 from .ops import (METHODS, kernel_family, quality, reload_knobs, sample,  # noqa: E402
-                  sample_host_batch, sort_axis)
+                  sample_host_batch, sort_axis, sort_perm)
 
 LIB_PATH = _os.path.join(_PKG, "lib", "libpcs_gpu.so")
 
 __all__ = [
     "fps", "afps", "npdu_fps", "npdu_afps", "exact_sort", "local_fps", "coverage_radius",
     "separation", "quality", "read_cloud", "write_cloud",
-    "sample", "sort_axis", "sample_host_batch", "kernel_family", "reload_knobs", "METHODS",
+    "sample", "sort_axis", "sort_perm", "sample_host_batch", "kernel_family", "reload_knobs", "METHODS",
     "LIB_PATH",
 ]

@@ -297,9 +297,11 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
   // kernels overlap on the worker streams.)
   std::vector<int64_t> bounds{0};
   {
-    // default: one chunk per ~4 MiB of input, at most 8 (small batches are
-    // dominated by per-chunk API and launch overhead, not by the copy)
-    const int64_t by_size = static_cast<int64_t>((cloud_bytes * B) >> 22);
+    // default: one chunk per ~1.5 MiB of input, at most 8 (small batches
+    // are dominated by per-chunk API and launch overhead, not by the copy;
+    // r02 sweep, tools/e2e_parts.py: cfg3 (6.3 MB) 0.288 ms in one chunk vs
+    // 0.255 in four, cfg4 (50 MB) best at 8)
+    const int64_t by_size = static_cast<int64_t>((cloud_bytes * B) / (size_t(3) << 19));
     const int64_t def = std::max<int64_t>(1, std::min<int64_t>(8, by_size));
     const int64_t nu = std::min<int64_t>(std::min<int64_t>(B, chunks > 0 ? chunks : def), kEvents - 4);
     for (int64_t i = 1; i <= nu; ++i) bounds.push_back(B * i / nu);
@@ -313,12 +315,11 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
   cudaStream_t copy = ds.copy;
   cudaStream_t* work = ds.work;
   void* ws = nullptr;
-  size_t off_xyz = 0, off_srt = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
+  size_t off_xyz = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
   if (e == cudaSuccess) {
     size_t bytes = 0;
     auto take = [&](size_t& off, size_t len) { off = bytes; bytes += (len + 255) & ~size_t(255); };
     take(off_xyz, cloud_bytes * B);
-    take(off_srt, sort_axis >= 0 ? cloud_bytes * B : 0);
     take(off_perm, sort_axis >= 0 ? 4 * static_cast<size_t>(N) * B : 0);
     take(off_idx, isize * static_cast<size_t>(C) * B);
     take(off_sec, ha->out_sector ? 4 * static_cast<size_t>(C) * B : 0);
@@ -342,15 +343,13 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
     if (e == cudaSuccess) e = cudaEventRecord(ready, copy);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(w, ready, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(w, seeds_ready, 0);
-    const void* src = dx;
     int32_t* dperm = reinterpret_cast<int32_t*>(base + off_perm) + N * b0;
-    if (e == cudaSuccess && sort_axis >= 0) {
-      char* ds = base + off_srt + cloud_bytes * b0;
-      e = launch_sort(ha->coord_dtype, dx, nb, N, sort_axis, ds, dperm, w);
-      src = ds;
-    }
+    // the sort writes only the permutation; the sampler gathers through it
+    if (e == cudaSuccess && sort_axis >= 0)
+      e = launch_sort(ha->coord_dtype, dx, nb, N, sort_axis, nullptr, dperm, w);
     pcs_gpu_args a = *ha;
-    a.xyz = src;
+    a.xyz = dx;
+    a.perm = sort_axis >= 0 ? dperm : nullptr;
     a.batch = nb;
     a.seeds = ha->seeds ? reinterpret_cast<const uint64_t*>(base + off_seed) + b0 : nullptr;
     a.out_indices = base + off_idx + isize * C * b0;
@@ -402,11 +401,10 @@ int host_sector_slice(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
   if (e != cudaSuccess) return fail_to(e, "", err);
   std::lock_guard<std::mutex> lock(dsp->mu);
   cudaStream_t st = dsp->work[0];
-  size_t bytes = 0, off_srt = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
+  size_t bytes = 0, off_perm = 0, off_idx = 0, off_sec = 0, off_st = 0, off_seed = 0;
   auto take = [&](size_t& off, size_t len) { off = bytes; bytes += (len + 255) & ~size_t(255); };
   size_t off_xyz = 0;
   take(off_xyz, cloud_bytes);
-  take(off_srt, sort_axis >= 0 ? cloud_bytes : 0);
   take(off_perm, sort_axis >= 0 ? 4 * static_cast<size_t>(N) : 0);
   take(off_idx, isize * static_cast<size_t>(c));
   take(off_sec, 4 * static_cast<size_t>(c));
@@ -419,14 +417,14 @@ int host_sector_slice(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
   e = cudaMemcpyAsync(base + off_xyz, ha->xyz, cloud_bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && ha->seeds)
     e = cudaMemcpyAsync(base + off_seed, ha->seeds, 8, cudaMemcpyHostToDevice, st);
-  const char* src = base + off_xyz;
   int32_t* dperm = reinterpret_cast<int32_t*>(base + off_perm);
-  if (e == cudaSuccess && sort_axis >= 0) {
-    e = launch_sort(ha->coord_dtype, base + off_xyz, 1, N, sort_axis, base + off_srt, dperm, st);
-    src = base + off_srt;
-  }
+  if (e == cudaSuccess && sort_axis >= 0)
+    e = launch_sort(ha->coord_dtype, base + off_xyz, 1, N, sort_axis, nullptr, dperm, st);
   pcs_gpu_args a = *ha;
-  a.xyz = src + csize * 3 * static_cast<size_t>(point_lo);
+  // the slice of the sorted order: through the permutation (storage
+  // indices of the whole cloud), or the storage slice when not sorting
+  a.xyz = base + off_xyz + (sort_axis >= 0 ? 0 : csize * 3 * static_cast<size_t>(point_lo));
+  a.perm = sort_axis >= 0 ? dperm + point_lo : nullptr;
   a.batch = 1;
   a.n = point_hi - point_lo;
   a.m = m;
@@ -460,6 +458,7 @@ int check_host_args(const pcs_gpu_args* ha, int32_t sort_axis, const char* who) 
   if (ha->batch < 0) { set_error(std::string(who) + ": batch must be >= 0"); return PCS_ERR_INVALID_ARGUMENT; }
   if (sort_axis < -1 || sort_axis > 2) { set_error("axis must be x, y, or z"); return PCS_ERR_INVALID_ARGUMENT; }
   if (ha->batch > 0 && (!ha->xyz || !ha->out_indices)) { set_error(std::string(who) + ": null buffer"); return PCS_ERR_INVALID_ARGUMENT; }
+  if (ha->perm) { set_error(std::string(who) + ": perm is a device-call field; use sort_axis"); return PCS_ERR_INVALID_ARGUMENT; }
   return PCS_OK;
 }
 

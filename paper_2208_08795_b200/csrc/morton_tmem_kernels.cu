@@ -106,7 +106,12 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
     const int last_R = (srows_local - 1) * CS + rank;
     held = (srows_local - 1) * 32 + min(32, n - last_R * 32);
   }
-  const float* cloud = static_cast<const float*>(p.xyz) + (b * p.N + g.begin) * 3;
+  // sector point j: storage order, or through the sort permutation
+  const float* cloud_b = static_cast<const float*>(p.xyz) + b * p.N * 3;
+  const int* perm_s = p.perm ? p.perm + b * p.N + g.begin : nullptr;
+  auto pt = [&](long long j) -> const float* {
+    return cloud_b + 3LL * (perm_s ? static_cast<long long>(__ldg(perm_s + j)) : g.begin + j);
+  };
 
   // ---- 1. bounding box of the CTA's points (read from global / L2)
   {
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
     for (int jl = threadIdx.x; jl < np; jl += T) {
       const int gj = to_sector(jl);
       if ((jl >> 5) < srows_local && gj < n) {
-        const float* q = cloud + 3LL * gj;
+        const float* q = pt(gj);
         const float x = q[0], y = q[1], z = q[2];
         x0 = fminf(x0, x); x1 = fmaxf(x1, x);
         y0 = fminf(y0, y); y1 = fmaxf(y1, y);
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       const int gj = to_sector(jl);
       uint32_t cell = kNoIndex;
       if ((jl >> 5) < srows_local && gj < n) {
-        const float* q = cloud + 3LL * gj;
+        const float* q = pt(gj);
         auto qz = [&](float c, float c0) {
           const float t = fminf(fmaxf((c - c0) * sc, 0.f), 1023.f);
           return spread3(static_cast<uint32_t>(t));
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
       uint32_t o = kNoIndex;
       if (valid) {
         const int gj = to_sector(static_cast<int>(jl));
-        const float* q = cloud + 3LL * gj;
+        const float* q = pt(gj);
         x = q[0]; y = q[1]; z = q[2];
         o = static_cast<uint32_t>(gj);
       }
@@ -255,7 +260,8 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   gs.s = s;
   gs.g = g;
   int cur = first_point(p, gs);  // sector-local
-  float pfx = cloud[3LL * cur], pfy = cloud[3LL * cur + 1], pfz = cloud[3LL * cur + 2];
+  const float* pc = pt(cur);
+  float pfx = pc[0], pfy = pc[1], pfz = pc[2];
   double px = pfx, py = pfy, pz = pfz;
   const long long out_base = b * p.C + g.out_off;
   const long long index_off = g.begin + p.index_base;

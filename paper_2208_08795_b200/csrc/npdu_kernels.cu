@@ -105,11 +105,10 @@ __global__ void __launch_bounds__(768) npdu_warp_kernel(const SampleParams p) {
   auto Z = [&](int j) -> CT { if constexpr (GC) return __ldg(gsrc + 3 * min(j, n - 1) + 2); else return zs[j]; };
   if (sizeof(CT) < sizeof(double) && p.f64) __trap();  // fp32 staging is fp32-input only
   if constexpr (!GC) {
-    const long long off = (b * p.N + g.begin) * 3;
     if (p.f64)
-      stage_sector(static_cast<const double*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+      stage_sector_of<double>(p, b, g.begin, n, xs, ys, zs, lane, 32);
     else
-      stage_sector(static_cast<const float*>(p.xyz) + off, n, xs, ys, zs, lane, 32);
+      stage_sector_of<float>(p, b, g.begin, n, xs, ys, zs, lane, 32);
   }
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   for (int j = lane; j < np; j += 32) {
@@ -422,7 +421,7 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     float* ys = xs + NCAP;
     float* zs = ys + NCAP;
     unsigned* sampled = reinterpret_cast<unsigned*>(zs + NCAP);
-    stage_sector(static_cast<const float*>(p.xyz) + (b * p.N + g.begin) * 3, n, xs, ys, zs, lane, 32);
+    stage_sector_of<float>(p, b, g.begin, n, xs, ys, zs, lane, 32);
     const int rows = (n + 31) >> 5;
     for (int w = lane; w < rows + 8; w += 32) sampled[w] = 0u;
     // d = +inf on the sector, 0 on the pad rows

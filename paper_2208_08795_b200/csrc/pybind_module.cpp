@@ -266,7 +266,7 @@ PYBIND11_MODULE(_core, m) {
            std::int64_t c, std::int64_t mm, std::int64_t k, int seed_policy, std::uint64_t seed,
            std::uintptr_t seeds, int index_dtype, std::uintptr_t out_idx, std::uintptr_t out_sector,
            std::uintptr_t out_stats, std::uintptr_t stream, std::int64_t index_base,
-           std::int64_t sector_base) {
+           std::int64_t sector_base, std::uintptr_t perm) {
           pcs_gpu_args a{};
           a.index_base = index_base;
           a.sector_base = sector_base;
@@ -285,13 +285,14 @@ PYBIND11_MODULE(_core, m) {
           a.out_indices = reinterpret_cast<void*>(out_idx);
           a.out_sector = reinterpret_cast<std::int32_t*>(out_sector);
           a.out_stats = reinterpret_cast<std::uint64_t*>(out_stats);
+          a.perm = reinterpret_cast<const std::int32_t*>(perm);
           check(pcs_gpu_sample(&a, reinterpret_cast<void*>(stream)));
         },
         py::arg("method"), py::arg("coord_dtype"), py::arg("xyz"), py::arg("batch"), py::arg("n"),
         py::arg("c"), py::arg("m"), py::arg("k"), py::arg("seed_policy"), py::arg("seed"),
         py::arg("seeds"), py::arg("index_dtype"), py::arg("out_idx"), py::arg("out_sector"),
         py::arg("out_stats"), py::arg("stream"), py::arg("index_base") = 0,
-        py::arg("sector_base") = 0);
+        py::arg("sector_base") = 0, py::arg("perm") = 0);
   // the dispatch decision of pcs_gpu_sample (no device work)
   m.def("kernel_family",
         [](int method, int coord_dtype, std::int64_t batch, std::int64_t n, std::int64_t c,

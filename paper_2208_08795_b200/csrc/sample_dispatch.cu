@@ -1,4 +1,5 @@
 // Batched sampler entry: picks the kernel family per sector size and window.
+#include <algorithm>
 #include <initializer_list>
 
 #include "sampler_common.cuh"
@@ -73,6 +74,25 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
 
 }  // namespace pcsk
 
+namespace pcsk {
+
+// xyz[b, perm[b, i]] -> out[b, i]: the sorted copy, for the engines that
+// re-read coordinates from global memory (rows, Morton rows in shared
+// memory, streaming) instead of staging them once.
+template <typename T>
+__global__ void gather_sorted_kernel(const T* __restrict__ xyz, const int* __restrict__ perm,
+                                     long long N, long long total, T* __restrict__ out) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += 256LL * gridDim.x) {
+    const long long b = i / N;
+    const T* q = xyz + 3 * (b * N + __ldg(perm + i));
+    out[3 * i] = q[0];
+    out[3 * i + 1] = q[1];
+    out[3 * i + 2] = q[2];
+  }
+}
+
+}  // namespace pcsk
+
 namespace pcs_internal {
 
 namespace {
@@ -84,6 +104,7 @@ pcsk::SampleParams params_of(const pcs_gpu_args& a, long long* nmax) {
   *nmax = (a.n + M - 1) / M;
   pcsk::SampleParams p{};
   p.xyz = a.xyz;
+  p.perm = a.perm;
   p.f64 = a.coord_dtype == PCS_DTYPE_F64;
   p.B = a.batch;
   p.N = a.n;
@@ -109,12 +130,42 @@ pcsk::SampleParams params_of(const pcs_gpu_args& a, long long* nmax) {
 
 cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::string* msg) {
   long long nmax = 0;
-  const pcsk::SampleParams p = params_of(a, &nmax);
+  pcsk::SampleParams p = params_of(a, &nmax);
   if (a.out_stats) {
     cudaError_t e = cudaMemsetAsync(a.out_stats, 0, sizeof(uint64_t) * 4 * a.batch, stream);
     if (e != cudaSuccess) return e;
   }
-  return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+  if (!p.perm) return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+  // The staging engines gather through the permutation themselves; the
+  // engines that re-read coordinates from global memory get a sorted copy.
+  std::string fam;
+  {
+    pcsk::g_plan = &fam;
+    const cudaError_t pe = pcsk::dispatch(p, nmax, p.K > 0, nullptr, msg);
+    pcsk::g_plan = nullptr;
+    if (pe != cudaSuccess) return pe;
+  }
+  const bool stages = fam.rfind("fps_full_kernel", 0) == 0 || fam.rfind("npdu_", 0) == 0 ||
+                      fam.rfind("morton_tmem_kernel", 0) == 0;
+  if (stages) return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+  const size_t csize = p.f64 ? 8 : 4;
+  const long long total = p.B * p.N;
+  void* ws = nullptr;
+  cudaError_t e = workspace_alloc(&ws, csize * 3 * static_cast<size_t>(total), stream);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(148 * 8, (total + 255) / 256));
+  if (p.f64)
+    pcsk::gather_sorted_kernel<double><<<grid, 256, 0, stream>>>(
+        static_cast<const double*>(p.xyz), p.perm, p.N, total, static_cast<double*>(ws));
+  else
+    pcsk::gather_sorted_kernel<float><<<grid, 256, 0, stream>>>(
+        static_cast<const float*>(p.xyz), p.perm, p.N, total, static_cast<float*>(ws));
+  e = cudaGetLastError();
+  p.xyz = ws;
+  p.perm = nullptr;
+  if (e == cudaSuccess) e = pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
+  const cudaError_t e2 = cudaFreeAsync(ws, stream);
+  return e != cudaSuccess ? e : e2;
 }
 
 int plan_sample(const pcs_gpu_args& a, std::string* name, std::string* msg) {

@@ -40,6 +40,12 @@ namespace pcsk {
 
 struct SampleParams {
   const void* xyz;
+  // optional (B, N) sort permutation: sorted position -> storage index. When
+  // set, the clouds are sampled in that order (sector point j of cloud b is
+  // xyz[b, perm[b, begin + j]]): exact_sort's gather (proj/src/order.cpp:
+  // 19-21) fused into the sampler's staging, so the sort writes only the
+  // permutation and nobody writes / re-reads a sorted copy of the cloud.
+  const int* perm;
   int f64;
   long long B, N, C, M, K;  // K == 0: full window
   int random_first;
@@ -105,6 +111,57 @@ __device__ __forceinline__ void stage_sector(const Tin* __restrict__ src, int n,
   for (int e = e0 + t; e < 3 * n; e += nthreads) put(e, src[e]);
 }
 
+// Staging through the sort permutation: point j of the sector is storage
+// point perm_sector[j] of `cloud` (the cloud's first point).
+template <typename Tin, typename CT>
+__device__ __forceinline__ void stage_sector_perm(const Tin* __restrict__ cloud,
+                                                  const int* __restrict__ perm_sector, int n,
+                                                  CT* xs, CT* ys, CT* zs, int t, int nthreads) {
+  // four points in flight per thread: the permutation loads, then the
+  // twelve coordinate loads (L2 gathers), then the stores
+  int j = t;
+  for (; j + 3 * nthreads < n; j += 4 * nthreads) {
+    int i[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) i[u] = __ldg(perm_sector + j + u * nthreads);
+    Tin v[4][3];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const Tin* q = cloud + 3LL * i[u];
+      v[u][0] = __ldg(q);
+      v[u][1] = __ldg(q + 1);
+      v[u][2] = __ldg(q + 2);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jj = j + u * nthreads;
+      xs[jj] = static_cast<CT>(v[u][0]);
+      ys[jj] = static_cast<CT>(v[u][1]);
+      zs[jj] = static_cast<CT>(v[u][2]);
+    }
+  }
+  for (; j < n; j += nthreads) {
+    const Tin* q = cloud + 3LL * __ldg(perm_sector + j);
+    const Tin x = __ldg(q), y = __ldg(q + 1), z = __ldg(q + 2);
+    xs[j] = static_cast<CT>(x);
+    ys[j] = static_cast<CT>(y);
+    zs[j] = static_cast<CT>(z);
+  }
+}
+
+// Stage a sector [begin, begin + n) of cloud b into shared SoA, in storage
+// order or through p.perm.
+template <typename Tin, typename CT>
+__device__ __forceinline__ void stage_sector_of(const SampleParams& p, long long b,
+                                                long long begin, int n, CT* xs, CT* ys, CT* zs,
+                                                int t, int nthreads) {
+  const Tin* cloud = static_cast<const Tin*>(p.xyz) + b * p.N * 3;
+  if (p.perm)
+    stage_sector_perm(cloud, p.perm + b * p.N + begin, n, xs, ys, zs, t, nthreads);
+  else
+    stage_sector(cloud + begin * 3, n, xs, ys, zs, t, nthreads);
+}
+
 template <int W>
 __device__ __forceinline__ void group_sync(int gid) {
   if constexpr (W > 1)
@@ -153,11 +210,10 @@ __device__ __forceinline__ bool setup_group(const SampleParams& p, unsigned char
   gs.ys = gs.xs + p.nmax;
   gs.zs = gs.ys + p.nmax;
   gs.cand = reinterpret_cast<uint4*>(base + size_t(24) * p.nmax);
-  const long long off = (gs.b * p.N + gs.g.begin) * 3;
   if (p.f64)
-    stage_sector(static_cast<const double*>(p.xyz) + off, gs.g.n, gs.xs, gs.ys, gs.zs, t, W * 32);
+    stage_sector_of<double>(p, gs.b, gs.g.begin, gs.g.n, gs.xs, gs.ys, gs.zs, t, W * 32);
   else
-    stage_sector(static_cast<const float*>(p.xyz) + off, gs.g.n, gs.xs, gs.ys, gs.zs, t, W * 32);
+    stage_sector_of<float>(p, gs.b, gs.g.begin, gs.g.n, gs.xs, gs.ys, gs.zs, t, W * 32);
   if (p.out_sector)
     for (int i = t; i < gs.g.quota; i += W * 32)
       p.out_sector[gs.b * p.C + gs.g.out_off + i] = static_cast<int>(gs.s + p.sector_base);

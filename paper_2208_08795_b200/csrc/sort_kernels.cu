@@ -650,13 +650,62 @@ cudaError_t launch_device_radix(const T* xyz, long long batch, long long n, int 
 // long, poorly pipelined latency -- it bounded the first version of this
 // kernel, ncu short_scoreboard stalls on its consumers)
 __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+  // per bit: the bit as a predicate, its ballot, and the ballot or its
+  // complement folded into the running AND (4 instructions; the plain C++
+  // form compiled to ~7 per bit)
   unsigned peers = kFull;
 #pragma unroll
   for (int bit = 0; bit < 8; ++bit) {
-    const unsigned bb = __ballot_sync(kFull, (d >> bit) & 1u);
-    peers &= ((d >> bit) & 1u) ? bb : ~bb;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 m;\n\t"
+        "and.b32 m, %1, %2;\n\t"
+        "setp.ne.u32 p, m, 0;\n\t"
+        "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+        "@!p not.b32 m, m;\n\t"
+        "and.b32 %0, %0, m;\n\t}"
+        : "+r"(peers) : "r"(d), "r"(1u << bit));
   }
   return peers;
+}
+
+// Rank of each of the warp's E x 32 keys (slot e of lane l = segment
+// position 32 e + l) inside its digit run, packed two 16-bit ranks per rk
+// word. The lanes sharing a digit (peers) take consecutive ranks; the warp's
+// running count per digit in hw[] is advanced by one atomicAdd from the
+// peers' leader lane. A warp's shared-memory atomics complete in program
+// order, so slot e+1 sees slot e's counts and ranks follow storage order
+// (stable) without a warp barrier between slots: the slots of a group are
+// independent chains (ballots, then atomics, then the shuffles that
+// broadcast each leader's old count), not one serial read-modify-write.
+template <int E>
+__device__ __forceinline__ void warp_rank(const uint32_t (&key)[E], int shift, uint32_t* hw,
+                                          int lane, unsigned lt_mask, uint32_t (&rk)[E / 2]) {
+  constexpr int G = E < 4 ? E : 4;
+#pragma unroll
+  for (int e0 = 0; e0 < E; e0 += G) {
+    unsigned pm[G];
+    uint32_t old[G];
+    int ld[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const uint32_t d = (key[e0 + u] >> shift) & 255u;
+      pm[u] = digit_peers(d);
+      ld[u] = __ffs(pm[u]) - 1;
+      old[u] = 0;
+      // leader lane only, predicated (no divergent branch)
+      const uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(hw + d));
+      asm volatile("{\n\t.reg .pred p;\n\t"
+                   "setp.eq.s32 p, %1, %2;\n\t"
+                   "@p atom.shared.add.u32 %0, [%3], %4;\n\t}"
+                   : "+r"(old[u]) : "r"(lane), "r"(ld[u]), "r"(addr), "r"(__popc(pm[u]))
+                   : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int e = e0 + u;
+      const uint32_t r = __shfl_sync(kFull, old[u], ld[u]) + __popc(pm[u] & lt_mask);
+      if (e & 1) rk[e >> 1] |= r << 16; else rk[e >> 1] = r;
+    }
+  }
 }
 
 template <int NT, int E, int CS, int MINB>
@@ -694,17 +743,7 @@ __global__ void __launch_bounds__(NT, MINB)
     if (t == 0) identity = 0;
     __syncthreads();
     // rank inside the warp's digit run
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t d = (key[e] >> shift) & 255u;
-      const unsigned peers = digit_peers(d);
-      const uint32_t before = hw[d];
-      __syncwarp();
-      if ((peers & lt_mask) == 0) hw[d] = before + __popc(peers);
-      __syncwarp();
-      const uint32_t r = before + __popc(peers & lt_mask);
-      if (e & 1) rk[e >> 1] |= r << 16; else rk[e >> 1] = r;
-    }
+    warp_rank<E>(key, shift, hw, lane, lt_mask, rk);
     __syncthreads();
     // scan: thread (d, q) owns warps 8q .. 8q+7 of digit d
     const int d = t / P, q = t % P;
@@ -757,6 +796,22 @@ __global__ void __launch_bounds__(NT, MINB)
     const int skip = identity;
     __syncthreads();
     if (skip) continue;
+    if (CS == 1 && shift == 24) {
+      // last pass of a one-CTA cloud: write the outputs at their sorted
+      // positions directly
+      float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t dd = (key[e] >> shift) & 255u;
+        const uint32_t r = (e & 1) ? rk[e >> 1] >> 16 : rk[e >> 1] & 0xffffu;
+        const uint32_t pos = hw[dd] + r;
+        if (pos < N) {
+          if (out_perm) out_perm[b * N + pos] = static_cast<int>(idx[e]);
+          if (dst) gather_point(src, dst, pos, idx[e]);
+        }
+      }
+      return;
+    }
     // scatter
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -909,21 +964,29 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int i = t; i < 256 * NW; i += NT) hist[i] = 0;
     if (t == 0) identity = 0;
     __syncthreads();
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t d = (key[e] >> shift) & 255u;
-      const unsigned peers = digit_peers(d);
-      const uint32_t before = hw[d];
-      __syncwarp();
-      if ((peers & lt_mask) == 0) hw[d] = before + __popc(peers);
-      __syncwarp();
-      const uint32_t r = before + __popc(peers & lt_mask);
-      if (e & 1) rk[e >> 1] |= r << 16; else rk[e >> 1] = r;
-    }
+    warp_rank<E>(key, shift, hw, lane, lt_mask, rk);
     __syncthreads();
     if (cta_digit_offsets<NT>(hist, wsum, &identity, NP)) continue;
     const uint16_t* isrc = ib + cur * NP;
     uint16_t* idst = ib + (cur ^ 1) * NP;
+    if (CS == 1 && shift == 24) {
+      // last pass of a one-CTA cloud: the scatter position is the sorted
+      // position -- write the outputs there directly (no shared-memory
+      // round trip, no final pass over the buffer)
+      float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t dd = (key[e] >> shift) & 255u;
+        const uint32_t r = (e & 1) ? rk[e >> 1] >> 16 : rk[e >> 1] & 0xffffu;
+        const uint32_t pos = hw[dd] + r;
+        if (pos < N) {
+          const int from = isrc[lb + 32 * e];
+          if (out_perm) out_perm[b * N + pos] = from;
+          if (dst) gather_point(src, dst, pos, from);
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t dd = (key[e] >> shift) & 255u;
@@ -1049,6 +1112,7 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   // network (one or two CTAs per cloud, no cross-CTA scatter): 64 x 16K
   // 0.064 vs 0.082, 256 x 32K 0.53 vs 0.63.
   const bool radix_off = !pcs_internal::knobs().sort_radix;
+
   if (coord_dtype == PCS_DTYPE_F32 && !radix_off && (n <= 4096 || (batch <= 37 && n <= 65536))) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);

@@ -51,10 +51,31 @@ def sort_axis(xyz: torch.Tensor, axis="x"):
     return out, perm
 
 
+def sort_perm(xyz: torch.Tensor, axis="x") -> torch.Tensor:
+    """The permutation of :func:`sort_axis` alone (int32 (B, N)), without the
+    gathered copy -- what :func:`sample` passes to the sampler."""
+    if axis not in _AXES:
+        raise ValueError("axis must be x, y, or z")
+    x = _as_batch(xyz)
+    B, N = x.shape[0], x.shape[1]
+    perm = torch.empty((B, N), dtype=torch.int32, device=x.device)
+    _core.sort_device(1 if x.dtype == torch.float64 else 0, x.data_ptr(), B, N, _AXES[axis],
+                      0, perm.data_ptr(), _stream_handle(x.device))
+    return perm
+
+
+def sample_with_perm(xyz: torch.Tensor, perm: torch.Tensor, c: int, **kw):
+    """:func:`sample` of the clouds in the order of ``perm`` (int32 (B, N),
+    sorted position -> storage index, e.g. from :func:`sort_perm`): the
+    results of sampling the gathered copy, without the copy."""
+    return sample(xyz, c, _perm=perm, **kw)
+
+
 def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optional[int] = None,
            first: str = "fixed", seed: int = 0, seeds: Optional[torch.Tensor] = None,
            sort: Optional[str] = None, index_dtype: torch.dtype = torch.int32,
-           return_sector: bool = False, index_base: int = 0, sector_base: int = 0):
+           return_sector: bool = False, index_base: int = 0, sector_base: int = 0,
+           _perm: Optional[torch.Tensor] = None):
     """Sample ``c`` points from every cloud of ``xyz`` (``(B, N, 3)``).
 
     CUDA input: stream-ordered on the current stream, results on the device,
@@ -92,8 +113,16 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
         return tuple(torch.from_numpy(r) for r in res)
     x = _as_batch(xyz)
     perm = None
+    if _perm is not None:
+        if sort is not None:
+            raise ValueError("sort and a permutation are exclusive")
+        perm = _perm.to(device=x.device, dtype=torch.int32).contiguous()
+        if tuple(perm.shape) != (x.shape[0], x.shape[1]):
+            raise ValueError("perm must be (B, N)")
     if sort is not None:
-        x, perm = sort_axis(x, sort)
+        # the sort writes only the permutation; the sampler stages every
+        # sector through it (no sorted copy of the clouds is made)
+        perm = sort_perm(x, sort)
     B, N = x.shape[0], x.shape[1]
     dev = x.device
     if index_dtype not in (torch.int32, torch.int64):
@@ -112,11 +141,12 @@ def sample(xyz: torch.Tensor, c: int, method: str = "afps", m: int = 1, k: Optio
                         1 if first == "fixed" else 0, int(seed) & (2**64 - 1), seeds_ptr,
                         1 if index_dtype == torch.int64 else 0, idx.data_ptr(),
                         sector.data_ptr() if sector is not None else 0, stats.data_ptr(),
-                        _stream_handle(dev), int(index_base), int(sector_base))
+                        _stream_handle(dev), int(index_base), int(sector_base),
+                        perm.data_ptr() if perm is not None else 0)
     out = [idx, stats]
     if return_sector:
         out.append(sector)
-    if perm is not None:
+    if perm is not None and _perm is None:
         out.append(perm)
     return tuple(out)
 

@@ -958,3 +958,38 @@ def test_concurrent_callers_equal_serial(pcs):
                 assert a[2] == b[2]
             else:
                 np.testing.assert_array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("meth,B,n,c,m,k,dtype,knob", [
+    ("afps", 9, 3000, 700, 3, None, "float32", None),             # fps_full
+    ("npdu_afps", 3, 4096, 1024, 8, 65, "float32", None),         # npdu_wide
+    ("npdu_afps", 40, 4096, 1024, 8, 129, "float32", None),       # npdu_tmem
+    ("npdu_afps", 40, 4096, 1024, 8, 129, "float64", None),       # npdu_warp (fp64)
+    ("fps", 3, 9000, 700, 1, None, "float32", None),              # morton_tmem
+    ("npdu_fps", 2, 9000, 900, 1, 65, "float32", None),           # morton_tmem, window mode
+    ("fps", 2, 9000, 700, 1, None, "float64", None),              # morton_rows (fp64)
+    ("afps", 2, 5000, 600, 2, None, "float32", ("PCS_SAMPLER", "rows")),
+    ("afps", 2, 5000, 300, 2, None, "float32", ("PCS_SAMPLER", "stream")),
+])
+def test_sampling_through_the_sort_permutation(monkeypatch, meth, B, n, c, m, k, dtype, knob):
+    """sample(..., sort=axis) hands the sampler the sort permutation only
+    (pcs_gpu_args.perm: staging gathers through it, or a sorted copy for the
+    engines that re-read global memory); every kernel family gives exactly
+    the results of sampling the gathered sorted copy."""
+    import torch
+
+    import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import sample, sort_axis
+
+    if knob:
+        setknob(monkeypatch, *knob)
+    xyz = synth.primitives(B, n, 4, seed=n + B).astype(dtype)
+    xyz[:, 10:40] = xyz[:, 9:10]  # coincident points: ties in the sort and the argmax
+    x = torch.from_numpy(xyz).cuda()
+    fused = sample(x, c, method=meth, m=m, k=k, sort="y", first="random", seed=7,
+                   return_sector=True)
+    srt, perm = sort_axis(x, "y")
+    copy = sample(srt, c, method=meth, m=m, k=k, first="random", seed=7, return_sector=True)
+    assert torch.equal(fused[3], perm)
+    for a, b in zip(fused[:3], copy):
+        assert torch.equal(a, b), pcs.kernel_family(meth, n, m, k, dtype=dtype, batch=B)

@@ -29,7 +29,7 @@ def test_cabi_exports_every_declared_symbol(pcs):
     for name in names:
         assert hasattr(lib, name), name
     lib.pcs_abi_version.restype = ctypes.c_int
-    assert lib.pcs_abi_version() == 1
+    assert lib.pcs_abi_version() == 2
     lib.pcs_status_string.restype = ctypes.c_char_p
     assert lib.pcs_status_string(1) == b"invalid argument"
 

@@ -10,6 +10,6 @@ from paper_2208_08795_b200 import synth  # noqa: E402
 B, N = int(sys.argv[1]), int(sys.argv[2])
 x = torch.from_numpy(synth.uniform_cube(B, N, 1)).cuda()
 for _ in range(3):
-    pcs.sort_axis(x, "x")
+    pcs.sort_perm(x, "x")
 torch.cuda.synchronize()
 print("ok")
