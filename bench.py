@@ -244,7 +244,7 @@ def cpu_reference(w, xyz_sorted, budget_s=20.0, repeats=3):
             c = int(max(64, min(C, budget_s / max(per_pick, 1e-9))))
         best, idx = None, None
         for _ in range(max(1, repeats)):
-            t0 = time.perf_counter()
+            t0 = time.perf_counter()  # (ctypes call: no Python objects made inside)
             idx, _, _ = ref.sample(w["method"], pts, c, w["M"], w["K"] or 0,
                                    threads=workers if sectored else 1)
             dt = time.perf_counter() - t0
@@ -342,6 +342,22 @@ def run_reference_arm(args, w):
 
 
 # --------------------------------------------------------------------- GPU arm
+class no_gc:
+    """Python's cyclic GC paused inside a timed region (a full collection
+    stalled single timed calls by 5-30 ms); collected right before."""
+
+    def __enter__(self):
+        import gc
+
+        gc.collect()
+        gc.disable()
+
+    def __exit__(self, *a):
+        import gc
+
+        gc.enable()
+
+
 class Runner:
     """One workload on this rank's GPU: the step (sort + sample), the sort
     and the sampler alone, the host-buffer e2e call."""
@@ -393,14 +409,15 @@ class Runner:
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         out = None
-        for i in range(steps):
-            self._flush(i)
-            starts[i].record()
-            out = fn()
-            ends[i].record()
-            if per_step_sync:
-                torch.cuda.synchronize()
-        torch.cuda.synchronize()
+        with no_gc():
+            for i in range(steps):
+                self._flush(i)
+                starts[i].record()
+                out = fn()
+                ends[i].record()
+                if per_step_sync:
+                    torch.cuda.synchronize()
+            torch.cuda.synchronize()
         return sum(s.elapsed_time(e) for s, e in zip(starts, ends)), out
 
     def e2e(self, steps, warmup, world=1, dist=None):
@@ -425,20 +442,27 @@ class Runner:
             call()
             if i + 1 >= warmup and time.perf_counter() - t_warm > 0.5:
                 break
+        # and the timed loop's own sequence (flush, synchronize, call) a few
+        # times: its first run after a new input was measured at ~30 ms once
+        for i in range(3):
+            self._flush(i)
+            torch.cuda.synchronize()
+            call()
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         total = 0.0
         r = None
         per_call = []
-        for i in range(steps):
-            self._flush(i)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = call()
-            dt = time.perf_counter() - t0
-            per_call.append(dt * 1e3)
-            total += dt
+        with no_gc():
+            for i in range(steps):
+                self._flush(i)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = call()
+                dt = time.perf_counter() - t0
+                per_call.append(dt * 1e3)
+                total += dt
         e_ms = total * 1e3
         if dist is not None:
             t = torch.tensor([e_ms], dtype=torch.float64, device=self.dev)

@@ -468,23 +468,27 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     // stored 32 at a time; the sampled bitmap is only needed by the
     // all-zero slow path, which folds the outputs into it on demand
     int ob = cur;
+    const long long K = p.K;
+    const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
+    // dist_evals = the window sizes along the path: output t (t <= quota-2)
+    // is the pivot of iteration t+1, so each lane adds its buffered
+    // output's window when the block of 32 is stored (off the chain)
+    unsigned long long evals = 0;
     auto flush = [&](int t0, int cnt) {
       if (lane < cnt) {
         if (idx64) out64[t0 + lane] = index_off + ob;
         else out32[t0 + lane] = static_cast<int>(index_off + ob);
+        if (t0 + lane <= g.quota - 2)
+          evals += static_cast<unsigned long long>(min(n, ob + half_up) - max(0, ob - half_down));
       }
     };
     int marked = 0;  // outputs [0, marked) are in the bitmap
-    const long long K = p.K;
-    const int half_down = static_cast<int>(K / 2), half_up = static_cast<int>((K + 1) / 2);
     unsigned writes = 0;
-    unsigned long long evals = 0;
     for (int it = 1; it < g.quota; ++it) {
       const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
                    pz = static_cast<double>(zs[cur]);
       const int wb = cur >= half_down ? cur - half_down : 0;
       const int we = min(n, cur + half_up);
-      evals += static_cast<unsigned long long>(we - wb);
       // the RMAX rows from r_lo cover the window; near the sector's end
       // they are shifted down so they stay inside the allocated rows (the
       // extra rows are masked out and stored back unchanged)
@@ -500,15 +504,13 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
         dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
                         static_cast<double>(zs[jc]), px, py, pz);
       }
-      unsigned wmask = 0;
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
         const int j = j0 + 32 * q;
         const bool lower = j >= wb && j < we && dist[q] <= dj[q];
-        wmask |= lower ? (1u << q) : 0u;
+        writes += lower ? 1u : 0u;
         dj[q] = lower ? dist[q] : dj[q];
       }
-      writes += __popc(wmask);
       tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
@@ -568,11 +570,14 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     if (((g.quota - 1) & 31) != 31) flush((g.quota - 1) & ~31, ((g.quota - 1) & 31) + 1);
     tm_wait_st();
     const unsigned ws = __reduce_add_sync(kFull, writes);
+    // per-lane window sums (< 2^32 each: a lane holds <= quota/32 outputs
+    // of <= n points) -> the warp's
+    const unsigned long long ev = __reduce_add_sync(kFull, static_cast<unsigned>(evals));
     if (p.stats && lane == 0) {
       unsigned long long* st = p.stats + b * 4;
       const unsigned long long iters = static_cast<unsigned long long>(g.quota - 1);
       if (ws) atomicAdd(st + 1, static_cast<unsigned long long>(ws));
-      atomicAdd(st + 0, evals);
+      atomicAdd(st + 0, ev);
       atomicAdd(st + 2, iters * static_cast<unsigned long long>(n));
       atomicAdd(st + 3, iters);
     }

@@ -1129,9 +1129,12 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     if (n <= 32768) return pcsk::launch_radix_reg<512, 8, 8, 2>(x, batch, n, axis, o, out_perm, stream);
     return pcsk::launch_radix_reg<512, 8, 16, 2>(x, batch, n, axis, o, out_perm, stream);
   }
-  // a wave or more of large clouds: one 16K-point CTA per cloud (or a pair
-  // merging their halves), indices in shared memory (radix_cta_kernel)
-  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && batch >= 148 && n <= 32768) {
+  // more clouds (38+) of <= 32K points: one 16K-point CTA per cloud (or a
+  // pair merging their halves), indices in shared memory (radix_cta_kernel).
+  // With the leader-atomic ranking it beats the bitonic networks from 38
+  // clouds on (perm only, r02 tools/sort_sweep.py: 64x8K 0.035 -> 0.031 ms,
+  // 128x16K 0.094 -> 0.051, 48x32K 0.115 -> 0.064, 128x32K 0.223 -> 0.125)
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 32768) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
     if (n <= 8192) return pcsk::launch_radix_cta<512, 16, 1, 2>(x, batch, n, axis, o, out_perm, stream);
