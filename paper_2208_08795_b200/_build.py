@@ -26,7 +26,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SRCS = ["full_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "morton_kernels.cu",
+CU_SRCS = ["full_kernels.cu", "cluster_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "morton_kernels.cu",
            "morton_tmem_kernels.cu", "stream_kernels.cu",
            "sample_dispatch.cu",
            "sort_kernels.cu", "metrics_kernels.cu"]

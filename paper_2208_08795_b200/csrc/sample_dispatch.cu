@@ -53,7 +53,13 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   };
   const bool busy = p.B * p.M >= kBusySectors && nmax_sector > kMortonMinBusy && kn.morton_min < 0;
   cudaError_t e = cudaErrorNotSupported;
-  if (use_morton && (rows || nmax_sector > morton_min || (busy && morton_tmem))) e = morton_any();
+  // few full-window fp32 sectors (one wave of clusters): each spread over a
+  // cluster of up to 8 SMs (cluster_kernels.cu)
+  if (!windowed && !rows && kn.cluster && nmax_sector <= 8192)
+    e = run_cluster_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && use_morton &&
+      (rows || nmax_sector > morton_min || (busy && morton_tmem)))
+    e = morton_any();
   // windowed sectors past the TMEM NPDU kernel (> 4096 points, fp32): the
   // TMEM row engine in storage order, rows restricted to the window
   // (PCS_NPDU_BIG=0 keeps the warp / shared-memory row kernels)
@@ -146,7 +152,8 @@ cudaError_t launch_sample(const pcs_gpu_args& a, cudaStream_t stream, std::strin
     if (pe != cudaSuccess) return pe;
   }
   const bool stages = fam.rfind("fps_full_kernel", 0) == 0 || fam.rfind("npdu_", 0) == 0 ||
-                      fam.rfind("morton_tmem_kernel", 0) == 0;
+                      fam.rfind("morton_tmem_kernel", 0) == 0 ||
+                      fam.rfind("fps_cluster_kernel", 0) == 0;
   if (stages) return pcsk::dispatch(p, nmax, p.K > 0, stream, msg);
   const size_t csize = p.f64 ? 8 : 4;
   const long long total = p.B * p.N;

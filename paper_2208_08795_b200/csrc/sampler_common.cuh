@@ -285,5 +285,6 @@ cudaError_t run_rows_any(SampleParams p, long long nmax_sector, bool windowed, c
 cudaError_t run_morton_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_morton_tmem_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_stream_any(SampleParams p, long long nmax_sector, cudaStream_t st);
+cudaError_t run_cluster_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 
 }  // namespace pcsk
