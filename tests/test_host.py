@@ -49,6 +49,45 @@ def test_cabi_rejects_before_touching_the_device(pcs):
     assert lib.pcs_last_error() == b"partition_sectors: m exceeds point count"
 
 
+class _Args(ctypes.Structure):
+    """pcs_gpu_args (include/pcs_gpu.h, ABI v2)."""
+    _fields_ = [("method", ctypes.c_int32), ("coord_dtype", ctypes.c_int32),
+                ("xyz", ctypes.c_void_p), ("batch", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("c", ctypes.c_int64), ("m", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("seed_policy", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("seeds", ctypes.c_void_p), ("index_dtype", ctypes.c_int32),
+                ("out_indices", ctypes.c_void_p), ("out_sector", ctypes.c_void_p),
+                ("out_stats", ctypes.c_void_p), ("index_base", ctypes.c_int64),
+                ("sector_base", ctypes.c_int64), ("perm", ctypes.c_void_p)]
+
+
+def test_multi_device_and_plan_entries_validate_on_the_host(pcs):
+    """pcs_sample_host_multi / pcs_kernel_family reject bad arguments with
+    the reference's messages (or their own) before any device call."""
+    lib = ctypes.CDLL(pcs.LIB_PATH)
+    lib.pcs_last_error.restype = ctypes.c_char_p
+    pts = np.zeros((1, 10, 3), np.float32)
+    out = np.zeros(16, np.int32)
+    a = _Args(method=2, coord_dtype=0, xyz=pts.ctypes.data, batch=1, n=10, c=4, m=5, k=0,
+              seed_policy=1, index_dtype=0, out_indices=out.ctypes.data)
+    devs = (ctypes.c_int32 * 2)(0, 0)
+    assert lib.pcs_sample_host_multi(ctypes.byref(a), -1, None, devs, 2) == 1
+    assert lib.pcs_last_error() == b"allocate_samples: m exceeds sample count"
+    a.m = 2
+    assert lib.pcs_sample_host_multi(ctypes.byref(a), -1, None, devs, 0) == 1
+    assert lib.pcs_last_error() == b"pcs_sample_host_multi: need at least one device"
+    a.perm = out.ctypes.data
+    assert lib.pcs_sample_host_batch(ctypes.byref(a), -1, None, 0) == 1
+    assert b"perm is a device-call field" in lib.pcs_last_error()
+    a.perm = None
+    name = ctypes.create_string_buffer(64)
+    assert lib.pcs_kernel_family(ctypes.byref(a), name, 64) == 0
+    assert name.value == b"fps_full_kernel<1,1,1>"
+    a.c = 11
+    assert lib.pcs_kernel_family(ctypes.byref(a), name, 64) == 1
+    assert lib.pcs_last_error() == b"afps: c exceeds point count"
+
+
 BAD = [("fps", 0, 1, 1), ("fps", 11, 1, 1), ("afps", 4, 5, 1), ("afps", 11, 2, 1),
        ("afps", 4, 0, 1), ("npdu_afps", 4, 20, 3), ("npdu_fps", 4, 1, 0), ("npdu_afps", 4, 2, 0),
        ("npdu_afps", 10, 10, 0)]
