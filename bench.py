@@ -306,7 +306,20 @@ def arm_config(workload, w, world, mode):
             "l2": "flushed between steps (512 MiB write)",
             "parallelism": {"batch": f"clouds split over {world} GPU(s)",
                             "sector": f"sector-split x{world}",
+                            "replica": f"replicas x{world} (vanilla FPS on one cloud does "
+                                       "not shard: one global argmax per iteration)",
                             "weak": f"dp{world}"}[mode]}
+
+
+def run_mode(w, world):
+    """How the job spreads over `world` GPUs: a batch splits by cloud; one
+    AFPS / NPDU-AFPS cloud by sector run; one vanilla-FPS cloud (or fewer
+    sectors than GPUs) only by replica."""
+    if world <= 1 or w["B"] > 1:
+        return "batch"
+    if w["method"] in ("afps", "npdu_afps") and w["M"] >= world:
+        return "sector"
+    return "replica"
 
 
 def _loaded_native():
@@ -326,10 +339,11 @@ def run_reference_arm(args, w):
         return 0
     xyz = make_input(w)
     res, _, _ = cpu_reference(w, host_sorted(w, xyz), budget_s=8.0, repeats=args.steps)
-    mode = "sector" if (w["B"] == 1 and args.gpus > 1) else "batch"
+    mode = run_mode(w, args.gpus)
     line = {"metric": "sampled points/s", "value": res["value"], "unit": "sampled points/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak" if mode == "replica" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": arm_config(args.workload, w, args.gpus, mode),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -619,11 +633,13 @@ def main():
     # strong scaling: the job is the configured batch. Several clouds split
     # by cloud (BASELINE cfg4: 128 over 8 GPUs = 16 per GPU); one cloud
     # splits by sector run, every rank sorting the cloud itself
-    mode = "sector" if (B == 1 and world > 1) else "batch"
+    mode = run_mode(w, world)
     xyz_all = make_input(w)
     sh = None
     if mode == "sector":
         sh = shard.sector_shard(N, C, w["M"], world, rank)
+        xyz_host, b0 = xyz_all, 0
+    elif mode == "replica":
         xyz_host, b0 = xyz_all, 0
     else:
         b0, b1 = shard.split(B, world, rank)
@@ -648,7 +664,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     gpu_idx = out[0].cpu().numpy()
-    total_samples = B * C
+    total_samples = B * C * (world if mode == "replica" else 1)
     pts_per_s = total_samples / (ms_per_step * 1e-3)
 
     # ---- weak scaling beside it: every rank its own full batch
@@ -734,9 +750,9 @@ def main():
             "metric": "sampled points/s", "value": pts_per_s, "unit": "sampled points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak" if mode == "replica" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "clouds_per_s": B / (ms_per_step * 1e-3),
+            "clouds_per_s": B * (world if mode == "replica" else 1) / (ms_per_step * 1e-3),
             "config": arm_config(args.workload, w, world, mode),
             "gpu_launches": args.steps * launches_per_step(w),
             "dist_evals_per_step_rank0": evals_local,
