@@ -1116,6 +1116,11 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   if (coord_dtype == PCS_DTYPE_F32 && !radix_off && (n <= 4096 || (batch <= 37 && n <= 65536))) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
+    // <= one CTA per SM of 2K-point clouds: 512 threads x 4 keys (shorter
+    // per-warp rank chains) beat 256 x 8 (r02: 1x2048 and 16x2048 0.0143 ->
+    // 0.0123 ms; at 148 clouds equal)
+    if (n > 1024 && n <= 2048 && batch <= 148)
+      return pcsk::launch_radix_reg<512, 4, 1, 2>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 1024) return pcsk::launch_radix_reg<256, 4, 1, 4>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 2048) return pcsk::launch_radix_reg<256, 8, 1, 4>(x, batch, n, axis, o, out_perm, stream);
     if (n <= 4096) return pcsk::launch_radix_reg<512, 8, 1, 2>(x, batch, n, axis, o, out_perm, stream);
