@@ -25,6 +25,8 @@ LIB = os.path.join(LIBDIR, "libpcs_gpu.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# A/B builds only (tools/ab_versions.py): extra nvcc flags, e.g. -DPCS_...
+EXTRA_NVCC = os.environ.get("PCS_NVCC_EXTRA", "").split()
 
 CU_SRCS = ["full_kernels.cu", "cluster_kernels.cu", "npdu_kernels.cu", "rows_kernels.cu", "morton_kernels.cu",
            "morton_tmem_kernels.cu", "stream_kernels.cu",
@@ -68,7 +70,7 @@ def build(verbose=False):
         objs.append(o)
         if _newer(o, [s] + hdrs):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                         "-Xptxas", "-warn-spills", "-I", INC, "-c", s, "-o", o])
+                         "-Xptxas", "-warn-spills", *EXTRA_NVCC, "-I", INC, "-c", s, "-o", o])
     for src in CXX_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJDIR, src + ".o")

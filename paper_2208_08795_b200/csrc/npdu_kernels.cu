@@ -390,8 +390,15 @@ __host__ __device__ constexpr size_t tm_warp_smem(int ncap) {
   return (size_t(12) * ncap + 4 * ((ncap >> 5) + 8) + 15) & ~size_t(15);
 }
 
-// fp32 input, sectors <= NCAP <= 1024 points (one row maximum per lane)
-template <int RMAX, int NCAP>
+// Row-key forms of the TMEM kernel (see the cached-key comment inside):
+// exact (max d, index) keys, exact (max d, lane ballot) keys, or high-word
+// keys with an exact slow path. The high-word form issues the fewest
+// instructions (multi-wave launches, which are issue-bound); the exact index
+// form has the shortest argmax chain (one-wave launches, latency-bound).
+enum NpduKey { kKeyIndex = 0, kKeyBallot = 1, kKeyHigh = 2 };
+
+// fp32 input, sectors <= NCAP <= 4096 points (1-4 cached rows per lane)
+template <int RMAX, int NCAP, int KEY>
 __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
   static_assert(NCAP >= 32 * RMAX && NCAP <= 4096, "capacity");
   constexpr int RPL = NCAP > 1024 ? NCAP / 1024 : 1;  // rows per lane (row r: lane r % 32)
@@ -439,20 +446,26 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     if (p.out_sector)
       for (int i = lane; i < g.quota; i += 32)
         p.out_sector[b * p.C + g.out_off + i] = static_cast<int>(s + p.sector_base);
-    // cached row keys (row r = lane + 32 i): max d and either the ballot of
-    // the lanes holding it (index deferred to the winning row, kBallot) or
-    // the index itself. The ballot form saves instructions per row and wins
-    // with 5-row windows (cfg4 0.385 -> 0.357 ms); with 3-row windows the
-    // index form measured faster (cfg3 / cfg5 NPDU 8K kernels 0.059 / 0.116
-    // vs 0.065 / 0.123 ms).
-    constexpr bool kBallot = RMAX >= 5;
+    // cached row keys (row r = lane + 32 i), by KEY:
+    //  * kKeyIndex: (max d, lowest index holding it), exact;
+    //  * kKeyBallot: (max d, ballot of the lanes holding it), exact, the index
+    //    deferred to the winning row (rows order indices);
+    //  * kKeyHigh: the HIGH WORD of the row's max d and the ballot of the
+    //    lanes whose d carries it -- one redux.sync + one vote per touched
+    //    row. The high word orders distances except within a tie of high
+    //    words; the argmax is decided from these keys when that cannot
+    //    matter (a single candidate lane, or a tie at +inf: 0x7ff00000 is
+    //    +inf exactly, all such values are equal, lowest index wins) and
+    //    otherwise by an exact slow path that re-reads the candidate rows'
+    //    fp64 values from TMEM (measured: 3e-4 of cfg4's iterations).
     uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL];
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = lane + 32 * i;
       rm_hi[i] = r < rows ? kInfHi : 0u;
       rm_lo[i] = 0u;
-      rm_m[i] = kBallot ? (r < rows ? 1u : 0u) : (r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex);
+      rm_m[i] = KEY == kKeyIndex ? (r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex)
+                                 : (r < rows ? 1u : 0u);
     }
     GroupSetup gs;
     gs.b = b;
@@ -494,6 +507,8 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       // extra rows are masked out and stored back unchanged)
       const int r_lo = min(wb >> 5, max(rows - RMAX, 0));
       const int j0 = (r_lo << 5) + lane;
+      // j in [wb, we) <=> (unsigned)(j - wb) < we - wb
+      const uint32_t t0 = static_cast<uint32_t>(j0 - wb), wlen = static_cast<uint32_t>(we - wb);
       double dj[RMAX], dist[RMAX];
       tm_wait_st();
       tm_load_rows<RMAX>(tm + 2 * r_lo, dj);
@@ -506,62 +521,139 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
       }
 #pragma unroll
       for (int q = 0; q < RMAX; ++q) {
-        const int j = j0 + 32 * q;
-        const bool lower = j >= wb && j < we && dist[q] <= dj[q];
+        const bool lower = t0 + 32u * q < wlen && dist[q] <= dj[q];
         writes += lower ? 1u : 0u;
         dj[q] = lower ? dist[q] : dj[q];
       }
       tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
+      uint32_t mh, ml = 0u, j;
+      bool exact;
+      if constexpr (KEY != kKeyHigh) {
 #pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
-        uint32_t hi, lo, mk;
-        row_key_mask(dj[q], hi, lo, mk);
-        if constexpr (!kBallot) mk = static_cast<uint32_t>(((r_lo + q) << 5) + __ffs(mk) - 1);
-        store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
-      }
-      // this lane's best row (rows grow with i: strict > keeps the lowest),
-      // then the warp's: max d, lowest row among equals, its lowest lane
-      uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
-#pragma unroll
-      for (int i = 1; i < RPL; ++i)
-        if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
-          hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
+        for (int q = 0; q < RMAX; ++q) {
+          uint32_t hi, lo, mk;
+          row_key_mask(dj[q], hi, lo, mk);
+          if constexpr (KEY == kKeyIndex) mk = static_cast<uint32_t>(((r_lo + q) << 5) + __ffs(mk) - 1);
+          store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
         }
-      uint32_t j = mk;
-      if constexpr (!kBallot) {
-        warp_argmax(hi, lo, j);
+        // this lane's best row (rows grow with i: strict > keeps the lowest),
+        // then the warp's: max d, lowest row among equals, its lowest lane
+        uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
+#pragma unroll
+        for (int i = 1; i < RPL; ++i)
+          if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
+            hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
+          }
+        j = mk;
+        if constexpr (KEY == kKeyIndex) {
+          warp_argmax(hi, lo, j);
+        } else {
+          const uint32_t wh = __reduce_max_sync(kFull, hi);
+          const uint32_t wl = __reduce_max_sync(kFull, hi == wh ? lo : 0u);
+          const uint32_t mr = __reduce_min_sync(kFull, (hi == wh && lo == wl) ? rsel : kNoIndex);
+          const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
+          hi = wh;
+          lo = wl;
+          j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+        }
+        mh = hi;
+        ml = lo;
+        exact = (hi | lo) != 0u;
       } else {
-        const uint32_t mh = __reduce_max_sync(kFull, hi);
-        const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
-        const uint32_t mr = __reduce_min_sync(kFull, (hi == mh && lo == ml) ? rsel : kNoIndex);
-        const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
-        hi = mh;
-        lo = ml;
-        j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
-      }
-      if ((hi | lo) == 0u) {
-        // fold outputs [marked, it) into the bitmap: whole blocks from
-        // global memory, the current block from the lanes' buffers
-        const int t_blk = (it - 1) & ~31;
-        __syncwarp();
-        for (int t = marked + lane; t < t_blk; t += 32) {
-          const long long v = idx64 ? out64[t] : static_cast<long long>(out32[t]);
-          const int jl = static_cast<int>(v - index_off);
-          atomicOr(&sampled[jl >> 5], 1u << (jl & 31));
+#pragma unroll
+        for (int q = 0; q < RMAX; ++q) {
+          const uint32_t h = static_cast<uint32_t>(__double2hiint(dj[q]));
+          const uint32_t wk = __reduce_max_sync(kFull, h);
+          const uint32_t mk = __ballot_sync(kFull, h == wk);
+          const int r = r_lo + q;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i)
+            if (r == lane + 32 * i) {
+              rm_hi[i] = wk;
+              rm_m[i] = mk;
+            }
         }
-        if (lane <= ((it - 1) & 31) && t_blk + lane >= marked)
-          atomicOr(&sampled[ob >> 5], 1u << (ob & 31));
-        marked = it;
-        __syncwarp();
-        uint32_t jm = kNoIndex;
-        for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
-          const unsigned free_bits = ~sampled[w];
-          if (free_bits) {
-            const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
-            if (cand < static_cast<uint32_t>(n)) jm = cand;
+        // sector argmax on the high words: max, its lowest row, that row's
+        // lowest lane (rows order indices)
+        uint32_t wm, wr;
+        bool unique;
+        if constexpr (RPL == 1) {
+          mh = __reduce_max_sync(kFull, rm_hi[0]);
+          const uint32_t rb = __ballot_sync(kFull, rm_hi[0] == mh);
+          wr = static_cast<uint32_t>(__ffs(rb)) - 1u;
+          wm = __shfl_sync(kFull, rm_m[0], static_cast<int>(wr));
+          unique = (rb & (rb - 1u)) == 0u;
+        } else {
+          uint32_t lh = rm_hi[0], lm = rm_m[0], ls = static_cast<uint32_t>(lane);
+#pragma unroll
+          for (int i = 1; i < RPL; ++i)
+            if (rm_hi[i] > lh) { lh = rm_hi[i]; lm = rm_m[i]; ls = static_cast<uint32_t>(lane + 32 * i); }
+          int dup = 0;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) dup += rm_hi[i] == lh ? 1 : 0;
+          mh = __reduce_max_sync(kFull, lh);
+          const uint32_t rb = __ballot_sync(kFull, lh == mh);
+          const uint32_t rd = __ballot_sync(kFull, lh == mh && dup > 1);
+          wr = __reduce_min_sync(kFull, lh == mh ? ls : kNoIndex);
+          wm = __shfl_sync(kFull, lm, static_cast<int>(wr & 31u));
+          unique = (rb & (rb - 1u)) == 0u && rd == 0u;
+        }
+        j = (wr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+        exact = mh == kInfHi || (mh != 0u && unique && (wm & (wm - 1u)) == 0u);
+      }
+      if (!exact) {
+        uint32_t bh = mh, bl = ml;
+        if constexpr (KEY == kKeyHigh) {
+          // exact resolution over the candidate rows (a high-word tie, or
+          // every cached key 0): (max d, lowest index) from the fp64 values
+          tm_wait_st();
+          bh = bl = 0u;
+          j = kNoIndex;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            uint32_t cand = __ballot_sync(kFull, rm_hi[i] == mh && lane + 32 * i < rows);
+            while (cand) {
+              const int r = __ffs(cand) - 1 + 32 * i;
+              cand &= cand - 1u;
+              uint32_t t[2];
+              tm_ld(tm + 2 * r, t);
+              tm_wait_ld();
+              uint32_t h, l, mk;
+              // pad lanes past n hold d = 0 and are never written
+              row_key_mask(__hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0])), h, l, mk);
+              if (h > bh || (h == bh && l > bl) || j == kNoIndex) {
+                bh = h;
+                bl = l;
+                j = static_cast<uint32_t>((r << 5) + __ffs(mk) - 1);
+              }
+            }
           }
         }
-        j = __reduce_min_sync(kFull, jm);
+        if ((bh | bl) == 0u) {
+          // every distance is 0: lowest unsampled index (sampler.cpp:148-154);
+          // fold outputs [marked, it) into the bitmap: whole blocks from
+          // global memory, the current block from the lanes' buffers
+          const int t_blk = (it - 1) & ~31;
+          __syncwarp();
+          for (int t = marked + lane; t < t_blk; t += 32) {
+            const long long v = idx64 ? out64[t] : static_cast<long long>(out32[t]);
+            const int jl = static_cast<int>(v - index_off);
+            atomicOr(&sampled[jl >> 5], 1u << (jl & 31));
+          }
+          if (lane <= ((it - 1) & 31) && t_blk + lane >= marked)
+            atomicOr(&sampled[ob >> 5], 1u << (ob & 31));
+          marked = it;
+          __syncwarp();
+          uint32_t jm = kNoIndex;
+          for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+            const unsigned free_bits = ~sampled[w];
+            if (free_bits) {
+              const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
+              if (cand < static_cast<uint32_t>(n)) jm = cand;
+            }
+          }
+          j = __reduce_min_sync(kFull, jm);
+        }
       }
       cur = static_cast<int>(j);
       if (lane == (it & 31)) ob = cur;
@@ -588,6 +680,19 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tm_base), "r"(tm_cols));
 }
 
+template <int RMAX, int NCAP, int KEY>
+cudaError_t launch_npdu_tmem(SampleParams p, int G, int cols, size_t smem, cudaStream_t st) {
+  if (plan("npdu_tmem_kernel", {RMAX, NCAP, KEY})) return cudaSuccess;
+  auto kern = npdu_tmem_kernel<RMAX, NCAP, KEY>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  p.G = G;
+  const long long blocks = (p.B * p.M + G - 1) / G;
+  kern<<<static_cast<unsigned>(blocks), static_cast<unsigned>(32 * G), smem, st>>>(p, cols);
+  return cudaGetLastError();
+}
+
 template <int RMAX, int NCAP>
 cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   constexpr int cpw = tm_cols_per_warp(NCAP, RMAX);
@@ -600,7 +705,10 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   // More than one: CTAs of 4 warps (one TMEM column block) -- several per SM,
   // replaced as they finish, so the SMs stay near full occupancy without a
   // wave tail (cfg4 0.404 -> 0.386 ms, 256x32K M=16 1.01 -> 0.93 ms; one-wave
-  // batches keep the balanced single CTA: 256x4K 0.065 vs 0.10 ms).
+  // batches keep the balanced single CTA: 256x4K 0.065 vs 0.10 ms). More
+  // warps per SM than 4-warp CTAs give measured slower (cfg4: 6-warp CTAs,
+  // 18 warps/SM 0.359 ms, one 18-warp CTA 0.403, vs 0.341;
+  // profiles/r02_npdu_tmem_ab.log).
   const long long waves = (sectors + 148 * G - 1) / (148 * G);
   if (waves >= 2 && G >= 4)
     G = 4;
@@ -610,15 +718,14 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
   const size_t smem = wsm * G;
-  if (plan("npdu_tmem_kernel", {RMAX, NCAP})) return cudaSuccess;
-  auto kern = npdu_tmem_kernel<RMAX, NCAP>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  p.G = static_cast<int>(G);
-  const long long blocks = (sectors + G - 1) / G;
-  kern<<<static_cast<unsigned>(blocks), static_cast<unsigned>(32 * G), smem, st>>>(p, cols);
-  return cudaGetLastError();
+  // key form: multi-wave launches keep every SM's issue slots full, so the
+  // form with the fewest instructions wins (cfg4 0.358 -> 0.355 ms, 256x8K
+  // M=16 0.150 -> 0.144, 256x32K M=16 1.07 -> 0.96); a one-wave launch is
+  // bound by each warp's argmax chain, where the exact index form is the
+  // shortest (cfg3 0.082 vs 0.088 with high-word keys)
+  if (waves >= 2) return launch_npdu_tmem<RMAX, NCAP, kKeyHigh>(p, static_cast<int>(G), cols, smem, st);
+  if (RMAX >= 5) return launch_npdu_tmem<RMAX, NCAP, kKeyBallot>(p, static_cast<int>(G), cols, smem, st);
+  return launch_npdu_tmem<RMAX, NCAP, kKeyIndex>(p, static_cast<int>(G), cols, smem, st);
 }
 
 cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {

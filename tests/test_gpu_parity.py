@@ -490,6 +490,36 @@ def test_npdu_tmem_high_word_ties(oracle, monkeypatch, grid):
         np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("n,k,clouds", [(256, 65, 150), (2048, 65, 170), (4096, 129, 150)])
+@pytest.mark.parametrize("grid", [0, 8, 1 << 20])
+def test_npdu_tmem_high_word_keys_multiwave(reference, n, k, clouds, grid):
+    """Multi-wave TMEM NPDU launches take the high-word row keys
+    (npdu_tmem_kernel<R,NCAP,2>, 1, 2 and 4 cached rows per lane) -- under
+    ties: coarse grids (equal distances), distances a few ulps apart (high
+    words tie, low words differ) and uniform coordinates; every cloud
+    against the reference."""
+    import torch
+
+    import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import sample
+
+    m = 32
+    N, c = n * m, n * m // 4
+    fam = pcs.kernel_family("npdu_afps", N, m, k, batch=clouds, full=True)
+    assert fam.startswith("npdu_tmem_kernel<") and fam.endswith(",2>"), fam
+    rng = np.random.default_rng(grid + n)
+    xyz = synth.uniform_cube(clouds, N, n + grid)
+    if grid == 8:
+        xyz = (np.round(xyz * grid) / grid).astype(np.float32)
+    if grid == 1 << 20:
+        xyz = (1.0 + rng.integers(0, 4, xyz.shape) * 2.0 ** -22).astype(np.float32)
+    idx, st = sample(torch.from_numpy(xyz).cuda(), c, method="npdu_afps", m=m, k=k)
+    want_idx, want_st, _ = reference.sample_batch_f32("npdu_afps", xyz, c, m, k,
+                                                      workers=os.cpu_count())
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{n} {grid}")
+    np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+
+
 def test_streaming_engine_beyond_on_chip_sectors(oracle):
     """Sectors larger than every on-chip engine (d[] in global memory, one
     cooperative launch per sector, grid barrier per iteration): FPS and NPDU
