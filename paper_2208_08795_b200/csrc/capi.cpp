@@ -64,6 +64,7 @@ Knobs read_knobs() {
   if (const char* v = env("PCS_NPDU_TMEM")) k.npdu_tmem = v[0] != '0';
   if (const char* v = env("PCS_NPDU_BIG")) k.npdu_big = v[0] != '0';
   if (const char* v = env("PCS_SORT_RADIX")) k.sort_radix = v[0] != '0';
+  if (const char* v = env("PCS_SORT_BUCKET")) k.sort_bucket = v[0] != '0';
   if (const char* v = env("PCS_CLUSTER")) k.cluster = v[0] != '0';
   if (const char* v = env("PCS_CLUSTER_CS")) k.cluster_cs = std::atoi(v) >= 8 ? 8 : std::atoi(v) >= 4 ? 4 : 2;
   return k;

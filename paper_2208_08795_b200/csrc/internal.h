@@ -58,6 +58,7 @@ struct Knobs {
   bool npdu_tmem = true;      // PCS_NPDU_TMEM=0: one-warp NPDU keeps d in shared memory
   bool npdu_big = true;       // PCS_NPDU_BIG=0: no TMEM row engine for big windowed sectors
   bool sort_radix = true;     // PCS_SORT_RADIX=0: bitonic networks instead of on-chip radix
+  bool sort_bucket = true;    // PCS_SORT_BUCKET=0: 38+ clouds <= 32K take the radix CTA sort
   bool cluster = true;        // PCS_CLUSTER=0: no cluster-spread full-window kernel
   int cluster_cs = 8;         // PCS_CLUSTER_CS: largest cluster it may use (2, 4 or 8)
 };

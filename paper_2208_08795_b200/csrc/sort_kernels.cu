@@ -933,7 +933,7 @@ __device__ __forceinline__ bool cta_digit_offsets(uint32_t* hist, uint32_t* wsum
 template <int NT, int E, int CS, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     radix_cta_kernel(const float* __restrict__ xyz, long long N, int axis,
-                     float* __restrict__ out_xyz, int* __restrict__ out_perm) {
+                     float* __restrict__ out_xyz, int* __restrict__ out_perm, int only_flagged) {
   constexpr int NW = NT / 32, NP = NT * E;
   static_assert(CS == 1 || CS == 2, "one CTA or a pair");
   static_assert(NP * CS <= 65536, "16-bit indices");
@@ -952,6 +952,13 @@ __global__ void __launch_bounds__(NT, MINB)
   const int lb = w * 32 * E + lane;  // this thread's first slot (striped)
   const long long gbase = static_cast<long long>(rank) * NP;
 
+  if (only_flagged) {
+    // second launch after bucket_sort_kernel: only the clouds it flagged
+    // (perm[0] = -1); both CTAs of a pair read the flag before either writes
+    const int f = out_perm[b * N];
+    if constexpr (CS > 1) cg::this_cluster().sync();
+    if (f != -1) return;
+  }
   uint32_t key[E], rk[E / 2];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -1072,7 +1079,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
 template <int NT, int E, int CS = 1, int MINB = 1>
 cudaError_t launch_radix_cta(const float* xyz, long long batch, long long n, int axis,
-                             float* out_xyz, int* out_perm, cudaStream_t st) {
+                             float* out_xyz, int* out_perm, cudaStream_t st, int only_flagged = 0) {
   constexpr int NW = NT / 32;
   // keys, [2] 16-bit indices, per-warp digit counts, warp sums (+ the
   // partner's keys for the 2-CTA merge)
@@ -1093,8 +1100,213 @@ cudaError_t launch_radix_cta(const float* xyz, long long batch, long long n, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm);
+  e = cudaLaunchKernelEx(&cfg, kern, xyz, n, axis, out_xyz, out_perm, only_flagged);
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// ------------------------------------------------------ value-bucket sort
+// Stable sort of one cloud per CTA without per-digit ranking passes. The
+// (order key, storage index) pairs are unique and ordered exactly as the
+// stable sort orders the points, so any placement that sorts them is the
+// stable order -- no pass needs to be stable itself:
+//   1. order keys; the cloud's min / max;
+//   2. bucket = a monotone image of the value: fma(v, s, c) with
+//      s = nb / (hi - lo), c = 2^23 - lo s, read as an integer (float bits
+//      of [2^22, 2^24) are consecutive integers), clamped to [0, nb) -- a
+//      correctly rounded fma never reverses an order, so the buckets
+//      partition the sorted sequence; each key's slot inside its bucket is
+//      the histogram atomicAdd's return value;
+//   3. exclusive scan of the counts; scatter (key, index) to
+//      start[bucket] + slot (any order inside a bucket);
+//   4. each bucket sorted in place by one thread (insertion sort of the
+//      pairs: ~1 + nb / N pairs per bucket on average);
+//   5. the indices copied out coalesced.
+// A bucket larger than `limit` (many equal or clustered keys) would make
+// step 4 slow: the CTA flags the cloud (perm[0] = -1) and
+// radix_cta_kernel (only_flagged) sorts it in a second launch; so do clouds
+// with a non-finite key. Clouds whose keys are all equal take the identity.
+// Shared memory: keys 4N | indices 2N | 16-bit bucket starts 2 nb; the
+// 32-bit histogram lives in the key region until the scatter overwrites it.
+// Clouds < 65536 points (16-bit indices and starts).
+__device__ __forceinline__ float key_value(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+template <int NT, int E, bool KEEP>
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) bucket_sort_kernel(const float* __restrict__ xyz,
+                                                             long long N, int axis, int nb, int limit,
+                                                             float* __restrict__ out_xyz,
+                                                             int* __restrict__ out_perm) {
+  constexpr int NW = NT / 32;
+  // E > 16: the keys do not stay in registers between the histogram and the
+  // scatter (1024 threads x 64 registers); the scatter re-reads them (L2)
+  constexpr bool kKeep = KEEP;
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int n = static_cast<int>(N);
+  uint32_t* sk = smem;                                                  // n keys
+  uint32_t* hist = smem;                                                // nb counts (before the scatter)
+  uint16_t* si = reinterpret_cast<uint16_t*>(smem + ((n + 1) & ~1));   // n indices
+  uint16_t* st = si + ((n + 1) & ~1);                                   // nb + 1 starts
+  __shared__ uint32_t red[3][NW];
+  const long long b = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const float* src = xyz + b * N * 3;
+  int* perm = out_perm + b * N;
+  float* dst = out_xyz ? out_xyz + b * N * 3 : nullptr;
+
+  uint32_t key[E], pk[E];
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int g = t + NT * e;
+    key[e] = g < n ? order_key(__ldg(src + 3LL * g + axis)) : 0u;
+    if (g < n) {
+      kmin = min(kmin, key[e]);
+      kmax = max(kmax, key[e]);
+    }
+  }
+  for (int i = t; i < nb; i += NT) hist[i] = 0u;
+  kmin = __reduce_min_sync(kFull, kmin);
+  kmax = __reduce_max_sync(kFull, kmax);
+  if (lane == 0) {
+    red[0][w] = kmin;
+    red[1][w] = kmax;
+  }
+  __syncthreads();
+  kmin = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
+  kmax = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
+  if (kmin == kmax) {
+    // every key equal: storage order is the stable order
+    for (int i = t; i < n; i += NT) {
+      perm[i] = i;
+      if (dst) gather_point(src, dst, i, i);
+    }
+    return;
+  }
+  const float vlo = key_value(kmin), vhi = key_value(kmax);
+  const float sc = static_cast<float>(nb) / (vhi - vlo);
+  const float c0 = __fsub_rn(8388608.0f, __fmul_rn(vlo, sc));
+  const bool finite = isfinite(vlo) && isfinite(vhi) && isfinite(sc) && isfinite(c0);
+  auto bucket = [&](uint32_t k) -> int {
+    const int q = static_cast<int>(__float_as_uint(__fmaf_rn(key_value(k), sc, c0))) - 0x4B000000;
+    return min(max(q, 0), nb - 1);
+  };
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int g = t + NT * e;
+    pk[e] = 0u;
+    if (g < n) {
+      const int bk = bucket(key[e]);
+      pk[e] = (static_cast<uint32_t>(bk) << 16) | atomicAdd(&hist[bk], 1u);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the counts (thread t owns a contiguous run) and the
+  // largest bucket
+  const int per = (nb + NT - 1) / NT, i0 = min(t * per, nb), i1 = min(i0 + per, nb);
+  uint32_t sum = 0u, big = 0u;
+  for (int i = i0; i < i1; ++i) {
+    const uint32_t c = hist[i];
+    sum += c;
+    big = max(big, c);
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += v;
+  }
+  big = __reduce_max_sync(kFull, big);
+  if (lane == 31) red[2][w] = inc;
+  if (lane == 0) red[0][w] = big;
+  __syncthreads();
+  uint32_t wb = lane < NW ? red[2][lane] : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, wb, o);
+    if (lane >= o) wb += v;
+  }
+  big = __reduce_max_sync(kFull, lane < NW ? red[0][lane] : 0u);
+  uint32_t run = (w > 0 ? __shfl_sync(kFull, wb, (w - 1) & 31) : 0u) + inc - sum;
+  for (int i = i0; i < i1; ++i) {
+    st[i] = static_cast<uint16_t>(run);
+    run += hist[i];
+  }
+  if (t == 0) st[nb] = static_cast<uint16_t>(n);
+  if (big > static_cast<uint32_t>(limit) || !finite) {
+    // radix_cta_kernel sorts this cloud (second launch)
+    if (t == 0) perm[0] = -1;
+    return;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int g = t + NT * e;
+    if (g < n) {
+      const uint32_t k = kKeep ? key[e] : order_key(__ldg(src + 3LL * g + axis));
+      const uint32_t pos = st[pk[e] >> 16] + (pk[e] & 0xffffu);
+      sk[pos] = k;
+      si[pos] = static_cast<uint16_t>(g);
+    }
+  }
+  __syncthreads();
+  // rank by position: thread t takes the pairs at positions t + NT e (a
+  // warp's lanes mostly share a bucket, so their scans have equal trip
+  // counts)
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int p = t + NT * e;
+    if (p < n) {
+      const uint32_t k = sk[p], g = si[p];
+      const int bk = bucket(k);
+      const uint32_t beg = st[bk], end = st[bk + 1];
+      uint32_t lt = 0u, eq = 0u, j = beg;
+#pragma unroll 1
+      for (; j + 1u < end; j += 2u) {
+        const uint32_t a = sk[j], c = sk[j + 1];
+        lt += static_cast<uint32_t>(a < k) + static_cast<uint32_t>(c < k);
+        eq += static_cast<uint32_t>(a == k) + static_cast<uint32_t>(c == k);
+      }
+      if (j < end) {
+        const uint32_t a = sk[j];
+        lt += static_cast<uint32_t>(a < k);
+        eq += static_cast<uint32_t>(a == k);
+      }
+      if (eq > 1u) {
+        // key ties: storage order among them
+#pragma unroll 1
+        for (uint32_t j = beg; j < end; ++j) lt += (sk[j] == k && si[j] < g) ? 1u : 0u;
+      }
+      pk[e] = ((beg + lt) << 16) | g;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (t + NT * e < n) si[pk[e] >> 16] = static_cast<uint16_t>(pk[e] & 0xffffu);
+  __syncthreads();
+  for (int i = t; i < n; i += NT) {
+    const int from = si[i];
+    perm[i] = from;
+    if (dst) gather_point(src, dst, i, from);
+  }
+}
+
+template <int NT, int E, bool KEEP = (E <= 16)>
+cudaError_t launch_bucket_sort(const float* xyz, long long batch, long long n, int axis,
+                               float* out_xyz, int* out_perm, cudaStream_t st) {
+  // buckets: N / 2 (N / 4 above 16K points) -- more buckets shorten the
+  // rank scans but cost more in the histogram and its scan (r02 sweep,
+  // 256 clouds: N/1, N/2, N/4 at 8K 0.040 / 0.034 / 0.034 ms, 16K 0.071 /
+  // 0.058 / 0.060, 32K - / 0.124 / 0.114)
+  const int nb = static_cast<int>(std::max<long long>(1, n > 16384 ? n / 4 : n / 2));
+  const size_t smem = sizeof(uint32_t) * ((n + 1) & ~1LL) + sizeof(uint16_t) * (((n + 1) & ~1LL) + nb + 2);
+  auto kern = bucket_sort_kernel<NT, E, KEEP>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<static_cast<unsigned>(batch), NT, smem, st>>>(xyz, n, axis, nb, 96, out_xyz, out_perm);
+  return cudaGetLastError();
 }
 
 }  // namespace pcsk
@@ -1134,11 +1346,35 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     if (n <= 32768) return pcsk::launch_radix_reg<512, 8, 8, 2>(x, batch, n, axis, o, out_perm, stream);
     return pcsk::launch_radix_reg<512, 8, 16, 2>(x, batch, n, axis, o, out_perm, stream);
   }
-  // more clouds (38+) of <= 32K points: one 16K-point CTA per cloud (or a
+  // more clouds (38+) of 4K-32K points, permutation requested: the value-
+  // bucket sort, one CTA per cloud (r02 sweep, perm only: 256 x 8K 0.045 ->
+  // 0.034 ms, 256 x 16K 0.096 -> 0.058, 256 x 32K 0.242 -> 0.116, 64 x 8K
+  // 0.027 -> 0.026; clouds <= 4K stay on radix_reg_kernel: 256 x 2K 0.018
+  // vs 0.022 bucketed), then radix_cta_kernel for the clouds it flagged.
+  // Without a permutation output, 38+ clouds of <= 32K points: one
+  // 16K-point CTA per cloud (or a
   // pair merging their halves), indices in shared memory (radix_cta_kernel).
   // With the leader-atomic ranking it beats the bitonic networks from 38
   // clouds on (perm only, r02 tools/sort_sweep.py: 64x8K 0.035 -> 0.031 ms,
   // 128x16K 0.094 -> 0.051, 48x32K 0.115 -> 0.064, 128x32K 0.223 -> 0.125)
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 32768 && out_perm &&
+      pcs_internal::knobs().sort_bucket) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    cudaError_t e;
+    // 16 keys per thread (32 above 16K; fewer threads with more keys each
+    // measured slower: 256 x 16K 0.058 -> 0.065 ms at 32 per thread)
+    if (n <= 8192) e = pcsk::launch_bucket_sort<512, 16>(x, batch, n, axis, o, out_perm, stream);
+    else if (n <= 16384) e = pcsk::launch_bucket_sort<1024, 16>(x, batch, n, axis, o, out_perm, stream);
+    else e = pcsk::launch_bucket_sort<1024, 32>(x, batch, n, axis, o, out_perm, stream);
+    if (e != cudaSuccess) return e;
+    const bool pair = batch * 2 <= 148;
+    if (n <= 8192 && pair) return pcsk::launch_radix_cta<256, 16, 2, 4>(x, batch, n, axis, o, out_perm, stream, 1);
+    if (n <= 8192) return pcsk::launch_radix_cta<512, 16, 1, 2>(x, batch, n, axis, o, out_perm, stream, 1);
+    if (n <= 16384 && pair) return pcsk::launch_radix_cta<512, 16, 2, 2>(x, batch, n, axis, o, out_perm, stream, 1);
+    if (n <= 16384) return pcsk::launch_radix_cta<1024, 16, 1, 1>(x, batch, n, axis, o, out_perm, stream, 1);
+    return pcsk::launch_radix_cta<1024, 16, 2, 1>(x, batch, n, axis, o, out_perm, stream, 1);
+  }
   if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 32768) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);

@@ -244,6 +244,37 @@ def test_sort_kernel_families(pcs, monkeypatch, radix):
             np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("n", [1500, 4096, 5000, 8192, 12000, 16384, 20000, 32768])
+def test_bucket_sort_and_flagged_fallback(pcs, n):
+    """The value-bucket sort (38+ clouds <= 32K, permutation requested) in
+    one batch with every kind of cloud: uniform keys, keys with exact
+    duplicates inside buckets (ties ordered by storage index), signed
+    zeros, a constant axis (identity), a huge bucket and infinities (both
+    flagged and re-sorted by the radix CTA kernel in the second launch) --
+    against numpy's stable argsort, perm and gathered copy, both launch
+    forms of the fallback (one CTA / a pair per cloud)."""
+    import torch
+
+    from paper_2208_08795_b200 import sort_axis, sort_perm
+
+    rng = np.random.default_rng(n)
+    for b in (40, 150):
+        xyz = rng.random((b, n, 3), dtype=np.float32)
+        xyz[1::6, :, 0] = np.round(xyz[1::6, :, 0] * n / 3) / (n / 3)   # duplicates, small buckets
+        xyz[2::6, ::5, 0] = -0.0
+        xyz[2::6, 1::5, 0] = 0.0
+        xyz[3::6, :, 0] = 0.25                                           # constant
+        xyz[4::6, : n // 2, 0] = 0.5                                     # one huge bucket
+        xyz[5::6, 7, 0] = np.inf
+        xyz[5::6, 8, 0] = -np.inf
+        x = torch.from_numpy(xyz).cuda()
+        want, order = synth.stable_sort_np(xyz, 0)
+        out, perm = sort_axis(x, 0)
+        np.testing.assert_array_equal(perm.cpu().numpy(), order, err_msg=f"{b}x{n}")
+        np.testing.assert_array_equal(out.cpu().numpy(), want)
+        np.testing.assert_array_equal(sort_perm(x, "x").cpu().numpy(), order)
+
+
 def test_exact_sort_dropin_fp32_keys(pcs):
     """pcs.exact_sort on float64 clouds whose axis column is fp32-exact sorts
     fp32 keys on the device and gathers the float64 points on the host: the
