@@ -80,6 +80,9 @@ for _b in (1, 148, 4096):
                                        K=129, sort=None)
 
 DEFAULT_WORKLOAD = "cfg4"
+# --eager: every step launched from Python (default: the step's launches are
+# captured once in a CUDA graph and replayed, no host work between them)
+EAGER = False
 # the `workloads` object of the default run: every BASELINE config
 SWEEP = (["cfg1", "cfg2", "cfg3", "cfg3-afps", "cfg3-fps", "cfg4"]
          + [f"cfg5-{v}-{n}" for n in (2048, 4096, 8192, 16384, 32768)
@@ -382,6 +385,8 @@ class Runner:
         self.xyz = torch.from_numpy(xyz_host).to(dev)
         self.sh = shard_spec  # sector shard of one large cloud, or None
         self.flush = None
+        self.eager = EAGER or shard_spec is not None
+        self.graphs, self.graph_errors = [], []
 
     def sample_sorted(self, xs):
         w, pcs, sh = self.w, self.pcs, self.sh
@@ -413,6 +418,36 @@ class Runner:
             self.flush = self.torch.empty(512 * 1024 * 1024 // 4, dtype=self.torch.float32,
                                           device=self.dev)
         self.flush.fill_(float(i))
+
+    def graphed(self, fn):
+        """`fn` captured once in a CUDA graph (the step's launches replayed
+        without host work between them) -> (replay, static outputs); falls
+        back to (fn, None) when the launches cannot be captured."""
+        torch = self.torch
+        if self.eager:
+            return fn, None
+        try:
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                fn()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                out = fn()
+            torch.cuda.synchronize()
+            self.graphs.append(g)
+
+            def replay():
+                g.replay()
+                return out
+
+            return replay, out
+        except Exception as exc:  # e.g. an engine that cannot be captured
+            torch.cuda.synchronize()
+            self.graph_errors.append(f"{type(exc).__name__}: {exc}")
+            return fn, None
 
     def timed(self, fn, steps, per_step_sync=False):
         """Sum of CUDA-event times of `fn` over `steps` calls, L2 flushed
@@ -496,6 +531,7 @@ class Runner:
         del dst
         nbytes = pinned.numel() * pinned.element_size()
         return {"ms_per_step": e_ms, "min_ms": min(per_call), "max_ms": max(per_call),
+                "median_ms": float(np.median(per_call)),
                 "h2d_floor_ms": min(h2d),
                 "h2d_gbps": nbytes / min(h2d) / 1e6, "h2d_bytes_per_step": int(nbytes),
                 "d2h_bytes_per_step": int(sum(t.nbytes if hasattr(t, "nbytes") else
@@ -534,22 +570,25 @@ def measure_workload(pcs, torch, dev, name, w, steps, warmup, xyz_host, cpu_budg
         out = r.step(r.xyz)
     torch.cuda.synchronize()
     evals = int(out[1][:, 0].sum().item())
-    ms, out = r.timed(lambda: r.step(r.xyz), steps)
+    ms, out = r.timed(r.graphed(lambda: r.step(r.xyz))[0], steps)
     ms /= steps
     gpu_idx = out[0].cpu().numpy()
+    eager_ms = r.timed(lambda: r.step(r.xyz), steps)[0] / steps
     sort_ms = 0.0
     xs = r.xyz
     perm = None
     if w["sort"]:
         # the step's sort: the permutation only (the sampler stages through it)
-        sort_ms = r.timed(lambda: pcs.sort_perm(r.xyz, w["sort"]), steps)[0] / steps
+        sort_ms = r.timed(r.graphed(lambda: pcs.sort_perm(r.xyz, w["sort"]))[0], steps)[0] / steps
         perm = pcs.sort_perm(r.xyz, w["sort"])
-    samp_ms = r.timed(lambda: r.sample_perm(xs, perm), steps)[0] / steps
+    samp_ms = r.timed(r.graphed(lambda: r.sample_perm(xs, perm))[0], steps)[0] / steps
     peak, _ = fp64_peak()
     hbm, _ = hbm_peak()
     kern = pcs.kernel_family(w["method"], w["N"], w["M"], w["K"], batch=w["B"])
     entry = {"ms_per_step": ms, "sampled_pts_per_s": w["B"] * w["C"] / (ms * 1e-3),
-             "clouds_per_s": w["B"] / (ms * 1e-3), "sort_ms": sort_ms, "sampler_ms": samp_ms,
+             "clouds_per_s": w["B"] / (ms * 1e-3), "eager_ms_per_step": eager_ms,
+             "launch": "cuda graph replay" if r.graphs else "eager",
+             "sort_ms": sort_ms, "sampler_ms": samp_ms,
              "kernel": kern, "dist_evals_per_step": evals,
              "fp64_frac_algorithmic": (8.0 * evals / (samp_ms * 1e-3) / 1e12 / peak)
              if peak else None}
@@ -606,10 +645,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-workloads", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every step from Python instead of replaying a CUDA graph")
     ap.add_argument("--workloads", default=None,
                     help="comma-separated subset of the sweep (default: every BASELINE config)")
     ap.add_argument("--workloads-budget", type=float, default=150.0)
     args = ap.parse_args()
+    global EAGER
+    EAGER = args.eager
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference_arm(args, w)
@@ -655,8 +698,12 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    step_fn = r.graphed(lambda: r.step(r.xyz))[0]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        ms, out = r.timed(lambda: r.step(r.xyz), args.steps)
+        ms, out = r.timed(step_fn, args.steps)
     if world > 1:
         dist.barrier()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -664,6 +711,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     gpu_idx = out[0].cpu().numpy()
+    # the same step launched eagerly from Python (host work between launches)
+    eager_ms = r.timed(lambda: r.step(r.xyz), args.steps)[0]
+    t = torch.tensor([eager_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    eager_ms = float(t.item()) / args.steps
     total_samples = B * C * (world if mode == "replica" else 1)
     pts_per_s = total_samples / (ms_per_step * 1e-3)
 
@@ -686,7 +739,7 @@ def main():
     # ---- sampler kernel alone (roofline): sort once, time only the sampler
     if sh is None:
         perm = pcs.sort_perm(r.xyz, w["sort"]) if w["sort"] else None
-        kern_ms = r.timed(lambda: r.sample_perm(r.xyz, perm), args.steps,
+        kern_ms = r.timed(r.graphed(lambda: r.sample_perm(r.xyz, perm))[0], args.steps,
                           per_step_sync=True)[0] / args.steps
     else:
         xs = pcs.sort_axis(r.xyz, w["sort"])[0] if w["sort"] else r.xyz
@@ -750,6 +803,8 @@ def main():
             "metric": "sampled points/s", "value": pts_per_s, "unit": "sampled points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
+            "launch": ("cuda graph replay of the captured step (sort + sampler launches)"
+                       if r.graphs else "eager"), "eager_ms_per_step": eager_ms,
             "scaling": "weak" if mode == "replica" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "clouds_per_s": B * (world if mode == "replica" else 1) / (ms_per_step * 1e-3),
