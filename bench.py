@@ -486,9 +486,14 @@ class Runner:
 
         # warm-up: at least W steps and 0.5 s -- the host link ramps up over
         # the first ~15 transfers after idling (tools/e2e_dbg.py)
+        # (each call's result is held until the next returns, as in the timed
+        # loop: two live result sets, so the pinned host allocator has grown to
+        # both before timing -- otherwise the second timed call paid a ~2 ms
+        # cudaHostAlloc, tools/e2e_dbg.py)
         t_warm = time.perf_counter()
+        r = None
         for i in range(max(warmup, 1000)):
-            call()
+            r = call()
             if i + 1 >= warmup and time.perf_counter() - t_warm > 0.5:
                 break
         # and the timed loop's own sequence (flush, synchronize, call) a few
@@ -496,12 +501,11 @@ class Runner:
         for i in range(3):
             self._flush(i)
             torch.cuda.synchronize()
-            call()
+            r = call()
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         total = 0.0
-        r = None
         per_call = []
         with no_gc():
             for i in range(steps):

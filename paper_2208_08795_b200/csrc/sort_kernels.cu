@@ -1364,7 +1364,10 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
     cudaError_t e;
     // 16 keys per thread (32 above 16K; fewer threads with more keys each
     // measured slower: 256 x 16K 0.058 -> 0.065 ms at 32 per thread)
-    if (n <= 8192) e = pcsk::launch_bucket_sort<512, 16>(x, batch, n, axis, o, out_perm, stream);
+    // (at most one cloud per SM: 8 keys per thread shorten each CTA's chain,
+    // 64 x 8K 0.026 -> 0.022 ms; a full wave keeps 16: 256 x 8K 0.034 vs 0.036)
+    if (n <= 8192 && batch <= 148) e = pcsk::launch_bucket_sort<1024, 8>(x, batch, n, axis, o, out_perm, stream);
+    else if (n <= 8192) e = pcsk::launch_bucket_sort<512, 16>(x, batch, n, axis, o, out_perm, stream);
     else if (n <= 16384) e = pcsk::launch_bucket_sort<1024, 16>(x, batch, n, axis, o, out_perm, stream);
     else e = pcsk::launch_bucket_sort<1024, 32>(x, batch, n, axis, o, out_perm, stream);
     if (e != cudaSuccess) return e;
