@@ -300,7 +300,10 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   // 16-slot form measured faster (r01 sweep: cfg5 FPS 2K 0.374 vs 0.400 ms;
   // AFPS M=4 at 8K 1.69 vs 1.33 ms, cfg1 0.283 vs 0.262 ms).
   const long long sectors = p.B * p.M;
-  const bool p8 = sectors >= 4 * 148 || sectors <= 148;
+  // (r02: 512-point sectors at ~7 per SM -- 1024 sectors, cfg3 AFPS and
+  // cfg5 AFPS M=4 at 2K -- run faster with 16 slots, 0.108 -> 0.094 ms; from
+  // 4096 sectors on the 8-slot form wins again, 0.333 vs 0.384 ms at 8K M=16)
+  const bool p8 = (sectors >= 4 * 148 && !(n <= 512 && sectors <= 2048)) || sectors <= 148;
   if (p8) {
     if (n <= 512) return run_full<8, 2, true>(p, st);
     if (n <= 1024) return run_full<8, 4, true>(p, st);
