@@ -113,6 +113,8 @@ typedef struct pcs_gpu_args {
 /* Stream-ordered batched sampling. `stream` is a cudaStream_t (NULL = legacy
  * default stream). Returns after the launches are enqueued. */
 int pcs_gpu_sample(const pcs_gpu_args* args, void* stream);
+/* The same entry under the name SURVEY.md §8(b) gives it. */
+int pcs_gpu_sample_batched(const pcs_gpu_args* args, void* stream);
 
 /* Stable ascending sort of every cloud along `axis` (0 x, 1 y, 2 z) with the
  * reference's operator< on the coordinate (-0.0 == +0.0, ties keep storage
@@ -216,6 +218,7 @@ void pcs_debug_reload_knobs(void);
 /* Last error message of the calling thread ("" after success). */
 const char* pcs_last_error(void);
 const char* pcs_status_string(int status);
+const char* pcs_gpu_status_string(int status); /* alias of pcs_status_string */
 int pcs_abi_version(void);
 
 #ifdef __cplusplus

@@ -190,6 +190,10 @@ int pcs_gpu_sample(const pcs_gpu_args* a, void* stream) {
   return e == cudaSuccess ? PCS_OK : cuda_fail(e, msg);
 }
 
+int pcs_gpu_sample_batched(const pcs_gpu_args* a, void* stream) { return pcs_gpu_sample(a, stream); }
+
+const char* pcs_gpu_status_string(int status) { return pcs_status_string(status); }
+
 int pcs_kernel_family(const pcs_gpu_args* a, char* name, size_t capacity) {
   clear_error();
   if (!a) { set_error("pcs_kernel_family: null args"); return PCS_ERR_INVALID_ARGUMENT; }

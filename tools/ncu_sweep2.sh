@@ -8,7 +8,7 @@ W=${@:-cfg1 cfg2 cfg3 cfg3-afps cfg3-fps cfg4 cfg5-fps-2048 cfg5-fps-4096 cfg5-f
 mkdir -p gpurun_out
 for w in $W; do
   for what in sampler sort; do
-    if [ $what = sampler ]; then rx="regex:fps_full|fps_cluster|npdu_|morton_|rows_kernel|stream_sector"; else rx="regex:radix|bitonic|rs_scatter"; fi
+    if [ $what = sampler ]; then rx="regex:fps_full|fps_cluster|npdu_|morton_|rows_kernel|stream_sector"; else rx="regex:bucket|radix|bitonic|rs_scatter"; fi
     timeout 900 ncu --set full --clock-control none -k "$rx" -s 2 -c 1 \
       -o gpurun_out/ncu2_${w}_$what -f python bench.py --workload $w --steps 1 --warmup 3 \
       --no-cpu-baseline --no-e2e --no-workloads > gpurun_out/ncu2_${w}_$what.log 2>&1
