@@ -731,7 +731,9 @@ def main():
         for _ in range(args.warmup):
             rw.step(rw.xyz)
         dist.barrier()
-        wms = rw.timed(lambda: rw.step(rw.xyz), args.steps)[0]
+        wfn = rw.graphed(lambda: rw.step(rw.xyz))[0]
+        dist.barrier()
+        wms = rw.timed(wfn, args.steps)[0]
         t = torch.tensor([wms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wms = float(t.item()) / args.steps

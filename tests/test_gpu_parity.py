@@ -244,15 +244,16 @@ def test_sort_kernel_families(pcs, monkeypatch, radix):
             np.testing.assert_array_equal(out.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("n", [1500, 4096, 5000, 8192, 12000, 16384, 20000, 32768])
+@pytest.mark.parametrize("n", [700, 1500, 4096, 5000, 8192, 12000, 16384, 20000, 32768])
 def test_bucket_sort_and_flagged_fallback(pcs, n):
-    """The value-bucket sort (38+ clouds <= 32K, permutation requested) in
-    one batch with every kind of cloud: uniform keys, keys with exact
-    duplicates inside buckets (ties ordered by storage index), signed
-    zeros, a constant axis (identity), a huge bucket and infinities (both
-    flagged and re-sorted by the radix CTA kernel in the second launch) --
-    against numpy's stable argsort, perm and gathered copy, both launch
-    forms of the fallback (one CTA / a pair per cloud)."""
+    """The value-bucket sort (permutation requested: <= 148 clouds of <= 4K
+    in 1024-thread CTAs, 38+ clouds of 4K-32K) in one batch with every kind
+    of cloud: uniform keys, keys with exact duplicates inside buckets (ties
+    ordered by storage index), signed zeros, a constant axis (identity), a
+    huge bucket and infinities (flagged and re-sorted by the radix CTA
+    kernel in a second launch, or ranked all-pairs inside the CTA for <= 4K
+    points) -- against numpy's stable argsort, perm and gathered copy, both
+    launch forms of the flagged fallback (one CTA / a pair per cloud)."""
     import torch
 
     from paper_2208_08795_b200 import sort_axis, sort_perm

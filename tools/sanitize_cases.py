@@ -23,13 +23,22 @@ pcs.sort_axis(torch.from_numpy(synth.uniform_cube(1, 70000, 2)).cuda(), "x")    
 pcs.sort_axis(torch.from_numpy(synth.uniform_cube(1, 300000, 2)).cuda(), "x")     # device radix
 big = torch.from_numpy(synth.uniform_cube(1, 20000, 5)).cuda()
 pcs.sample(big, 50, method="fps")                             # Morton TMEM cluster
+xs = torch.from_numpy(synth.uniform_cube(40, 8192, 6)).cuda()
+xs[1, :5000, 0] = 0.5                                         # a huge bucket: flagged
+pcs.sort_perm(xs, "x")                                        # bucket sort + flagged radix
+xm = torch.from_numpy(synth.uniform_cube(700, 4096, 7)).cuda()
+pcs.sample(xm, 1024, method="npdu_afps", m=4, k=129)          # NPDU TMEM, high-word keys
+pcs.sample(torch.from_numpy(synth.uniform_cube(1, 2048, 8)).cuda(), 300, method="fps")  # cluster
 import os
 os.environ["PCS_SAMPLER"] = "stream"
+pcs.reload_knobs()
 pcs.sample(x, 100, method="fps")                              # streaming engine
 os.environ["PCS_SAMPLER"] = "rows"
 os.environ["PCS_MORTON"] = "0"
+pcs.reload_knobs()
 pcs.sample(x, 100, method="npdu_fps", k=65)                   # slab rows
 del os.environ["PCS_SAMPLER"], os.environ["PCS_MORTON"]
+pcs.reload_knobs()
 pts = synth.random_cloud(500, 3)
 pcs.fps(pts, 50)
 pcs.npdu_afps(pts, 50, 5, 9)
