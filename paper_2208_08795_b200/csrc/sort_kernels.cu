@@ -1132,7 +1132,7 @@ __device__ __forceinline__ float key_value(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-template <int NT, int E, bool KEEP>
+template <int NT, int E, bool KEEP, bool QUAD>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) bucket_sort_kernel(const float* __restrict__ xyz,
                                                              long long N, int axis, int nb, int limit,
                                                              float* __restrict__ out_xyz,
@@ -1234,9 +1234,42 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) bucket_sort_ke
   }
   if (t == 0) st[nb] = static_cast<uint16_t>(n);
   if (big > static_cast<uint32_t>(limit) || !finite) {
-    // radix_cta_kernel sorts this cloud (second launch)
-    if (t == 0) perm[0] = -1;
-    return;
+    if constexpr (!QUAD) {
+      // radix_cta_kernel sorts this cloud (second launch)
+      if (t == 0) perm[0] = -1;
+      return;
+    } else {
+      // small clouds (<= 4 keys per thread): rank every pair against the
+      // whole cloud in place of the second launch (n^2 / NT compares per
+      // thread, a rare path)
+      static_assert(!QUAD || KEEP, "the quadratic fallback keeps the keys in registers");
+      __syncthreads();  // the histogram (key region) has been read
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (t + NT * e < n) sk[t + NT * e] = key[e];
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int g = t + NT * e;
+        if (g < n) {
+          const uint32_t k = key[e];
+          uint32_t r = 0u;
+#pragma unroll 4
+          for (int j = 0; j < n; ++j) {
+            const uint32_t kj = sk[j];
+            r += (kj < k || (kj == k && j < g)) ? 1u : 0u;
+          }
+          si[r] = static_cast<uint16_t>(g);
+        }
+      }
+      __syncthreads();
+      for (int i = t; i < n; i += NT) {
+        const int from = si[i];
+        perm[i] = from;
+        if (dst) gather_point(src, dst, i, from);
+      }
+      return;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -1292,7 +1325,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) bucket_sort_ke
   }
 }
 
-template <int NT, int E, bool KEEP = (E <= 16)>
+template <int NT, int E, bool KEEP = (E <= 16), bool QUAD = false>
 cudaError_t launch_bucket_sort(const float* xyz, long long batch, long long n, int axis,
                                float* out_xyz, int* out_perm, cudaStream_t st) {
   // buckets: N / 2 (N / 4 above 16K points) -- more buckets shorten the
@@ -1301,7 +1334,7 @@ cudaError_t launch_bucket_sort(const float* xyz, long long batch, long long n, i
   // 0.058 / 0.060, 32K - / 0.124 / 0.114)
   const int nb = static_cast<int>(std::max<long long>(1, n > 16384 ? n / 4 : n / 2));
   const size_t smem = sizeof(uint32_t) * ((n + 1) & ~1LL) + sizeof(uint16_t) * (((n + 1) & ~1LL) + nb + 2);
-  auto kern = bucket_sort_kernel<NT, E, KEEP>;
+  auto kern = bucket_sort_kernel<NT, E, KEEP, QUAD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -1325,6 +1358,19 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   // 0.064 vs 0.082, 256 x 32K 0.53 vs 0.63.
   const bool radix_off = !pcs_internal::knobs().sort_radix;
 
+  // at most one cloud per SM of <= 4K points, permutation requested: the
+  // value-bucket sort in 1024-thread CTAs (1-4 keys per thread; a cloud it
+  // cannot bucket falls back to in-CTA all-pairs ranks, no second launch).
+  // r02 perm-only: 16 x 2K 0.0124 -> 0.0103 ms, 148 x 2K 0.0144 -> 0.0103,
+  // 64 x 4K 0.0184 -> 0.0123 (vs radix_reg_kernel)
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 4096 && batch <= 148 && out_perm &&
+      pcs_internal::knobs().sort_bucket) {
+    const float* x = static_cast<const float*>(xyz);
+    float* o = static_cast<float*>(out_xyz);
+    if (n <= 1024) return pcsk::launch_bucket_sort<1024, 1, true, true>(x, batch, n, axis, o, out_perm, stream);
+    if (n <= 2048) return pcsk::launch_bucket_sort<1024, 2, true, true>(x, batch, n, axis, o, out_perm, stream);
+    return pcsk::launch_bucket_sort<1024, 4, true, true>(x, batch, n, axis, o, out_perm, stream);
+  }
   if (coord_dtype == PCS_DTYPE_F32 && !radix_off && (n <= 4096 || (batch <= 37 && n <= 65536))) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
