@@ -250,6 +250,151 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
   flush_stats<W>(p, gs, t, writes, evals);
 }
 
+// ------------------------------------------------------ tiny sectors
+// Sectors of <= NP points (AFPS with many sectors: M=256 at 2K-4K points):
+// one THREAD per sector runs the whole local FPS -- fp64 d in
+// registers (every loop unrolled over NP slots, nothing indexed
+// dynamically), coordinates (input precision) in shared memory, slot-major. A warp per sector (fps_full_kernel) spent
+// most of its time staging 8-32 points and synchronising 32 lanes for one
+// to seven iterations. Windowed calls take update_window as usual. OpStats
+// are summed over the warp before the atomics when its sectors share a cloud.
+template <int NP, typename CT>
+__global__ void __launch_bounds__(128) fps_tiny_kernel(const SampleParams p) {
+  const long long flat = static_cast<long long>(blockIdx.x) * 128 + threadIdx.x;
+  const long long total = p.B * p.M;
+  const bool active = flat < total;
+  const long long b = active ? flat / p.M : 0, s = active ? flat % p.M : 0;
+  const SectorGeom g = sector_geom(p.N, p.C, p.M, s);
+  const int n = active ? g.n : 0;
+  const CT* cloud = static_cast<const CT*>(p.xyz) + b * p.N * 3;
+  const int* permb = p.perm ? p.perm + b * p.N : nullptr;
+  // coordinates in shared memory, slot-major (slot i of thread t at
+  // i * 128 + t: conflict-free), d in registers
+  __shared__ CT sxyz[3][NP * 128];
+  CT* const X = sxyz[0] + threadIdx.x;
+  CT* const Y = sxyz[1] + threadIdx.x;
+  CT* const Z = sxyz[2] + threadIdx.x;
+  double d[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    d[i] = 0.0;
+    X[i * 128] = Y[i * 128] = Z[i * 128] = CT(0);
+    if (i < n) {
+      const long long jj = g.begin + i;
+      const long long src = permb ? static_cast<long long>(__ldg(permb + jj)) : jj;
+      X[i * 128] = __ldg(cloud + 3 * src);
+      Y[i * 128] = __ldg(cloud + 3 * src + 1);
+      Z[i * 128] = __ldg(cloud + 3 * src + 2);
+      d[i] = __longlong_as_double(0x7ff0000000000000LL);
+    }
+  }
+  unsigned writes = 0, evals = 0;
+  int quota = active ? g.quota : 0;
+  if (active) {
+    GroupSetup gs;
+    gs.b = b;
+    gs.s = s;
+    gs.g = g;
+    int cur = first_point(p, gs);
+    const long long obase = b * p.C + g.out_off;
+    const long long ioff = g.begin + p.index_base;
+    auto put = [&](int slot, int v) {
+      if (p.idx64) static_cast<long long*>(p.out_idx)[obase + slot] = ioff + v;
+      else static_cast<int*>(p.out_idx)[obase + slot] = static_cast<int>(ioff + v);
+      if (p.out_sector) p.out_sector[obase + slot] = static_cast<int>(s + p.sector_base);
+    };
+    put(0, cur);
+    uint32_t sampled = NP > 32 ? 0u : (1u << cur);
+    double px = 0.0, py = 0.0, pz = 0.0;
+    px = static_cast<double>(X[cur * 128]);
+    py = static_cast<double>(Y[cur * 128]);
+    pz = static_cast<double>(Z[cur * 128]);
+    const int half_down = static_cast<int>(p.K / 2), half_up = static_cast<int>((p.K + 1) / 2);
+    for (int it = 1; it < quota; ++it) {
+      int wb = 0, we = n;
+      if (p.K > 0) {
+        wb = cur >= half_down ? cur - half_down : 0;
+        we = min(n, cur + half_up);
+      }
+      evals += static_cast<unsigned>(we - wb);
+      unsigned long long best = 0;
+      int bi = -1;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        if (i >= wb && i < we) {
+          const double dist = dist2(static_cast<double>(X[i * 128]), static_cast<double>(Y[i * 128]),
+                                    static_cast<double>(Z[i * 128]), px, py, pz);
+          const bool lower = dist <= d[i];
+          writes += lower ? 1u : 0u;
+          d[i] = lower ? dist : d[i];
+        }
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[i]));
+        if (i < n && bits > best) {
+          best = bits;
+          bi = i;
+        }
+      }
+      if (best == 0ull) {
+        // every distance is 0: lowest unsampled index (sampler.cpp:148-154)
+        bi = -1;
+#pragma unroll
+        for (int i = NP - 1; i >= 0; --i)
+          if (i < n && !((sampled >> i) & 1u)) bi = i;
+      }
+      cur = bi;
+      px = static_cast<double>(X[cur * 128]);
+      py = static_cast<double>(Y[cur * 128]);
+      pz = static_cast<double>(Z[cur * 128]);
+      sampled |= 1u << cur;
+      put(it, cur);
+    }
+  }
+  if (p.stats) {
+    const unsigned iters = quota > 0 ? static_cast<unsigned>(quota - 1) : 0u;
+    const unsigned scans = iters * static_cast<unsigned>(n);
+    if (p.K == 0) evals = scans;
+    // one atomic per counter per warp when all its sectors belong to one cloud
+    const long long b0 = __shfl_sync(kFull, b, 0);
+    const bool same = __all_sync(kFull, !active || b == b0) && __shfl_sync(kFull, active, 0);
+    if (same) {
+      const unsigned ev = __reduce_add_sync(kFull, evals), wr = __reduce_add_sync(kFull, writes),
+                     sc = __reduce_add_sync(kFull, scans), itr = __reduce_add_sync(kFull, iters);
+      if ((threadIdx.x & 31) == 0) {
+        unsigned long long* st = p.stats + b0 * 4;
+        atomicAdd(st + 0, static_cast<unsigned long long>(ev));
+        if (wr) atomicAdd(st + 1, static_cast<unsigned long long>(wr));
+        atomicAdd(st + 2, static_cast<unsigned long long>(sc));
+        atomicAdd(st + 3, static_cast<unsigned long long>(itr));
+      }
+    } else if (active) {
+      unsigned long long* st = p.stats + b * 4;
+      atomicAdd(st + 0, static_cast<unsigned long long>(evals));
+      if (writes) atomicAdd(st + 1, static_cast<unsigned long long>(writes));
+      atomicAdd(st + 2, static_cast<unsigned long long>(scans));
+      atomicAdd(st + 3, static_cast<unsigned long long>(iters));
+    }
+  }
+}
+
+template <int NP, typename CT>
+cudaError_t run_tiny(SampleParams p, cudaStream_t st) {
+  if (plan("fps_tiny_kernel", {NP, sizeof(CT) * 8})) return cudaSuccess;
+  const long long blocks = (p.B * p.M + 127) / 128;
+  fps_tiny_kernel<NP, CT><<<static_cast<unsigned>(blocks), 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// many sectors of <= 16 points; a thread per sector (r02, 256 clouds:
+// AFPS M=256 at 2K (8 points) 0.062 -> 0.021 ms, at 4K (16 points) 0.070 ->
+// 0.039; at 32 points a warp per sector wins again: M=256 at 8K 0.085 vs
+// 0.092, M=64 at 2K 0.025 vs 0.045)
+cudaError_t run_tiny_any(SampleParams p, long long n, cudaStream_t st) {
+  if (p.trace || n > 16 || p.B * p.M < kTinyMinSectors || !pcs_internal::knobs().tiny)
+    return cudaErrorNotSupported;
+  if (p.f64) return n <= 8 ? run_tiny<8, double>(p, st) : run_tiny<16, double>(p, st);
+  return n <= 8 ? run_tiny<8, float>(p, st) : run_tiny<16, float>(p, st);
+}
+
 template <typename Kern>
 cudaError_t launch_groups(Kern kern, const char* name, std::initializer_list<long long> targs,
                           SampleParams p, int W, int G, cudaStream_t st) {

@@ -56,6 +56,7 @@ struct Knobs {
   long long morton_min = -1;  // PCS_MORTON_MIN: full-window Morton crossover (points)
   long long npdu_wide = -1;   // PCS_NPDU_WIDE: most sectors the W-warp NPDU form takes
   bool npdu_tmem = true;      // PCS_NPDU_TMEM=0: one-warp NPDU keeps d in shared memory
+  bool tiny = true;           // PCS_TINY=0: tiny sectors keep a warp each (fps_full_kernel)
   bool npdu_big = true;       // PCS_NPDU_BIG=0: no TMEM row engine for big windowed sectors
   bool sort_radix = true;     // PCS_SORT_RADIX=0: bitonic networks instead of on-chip radix
   bool sort_bucket = true;    // PCS_SORT_BUCKET=0: 38+ clouds <= 32K take the radix CTA sort

@@ -55,7 +55,8 @@ cudaError_t dispatch(SampleParams p, long long nmax_sector, bool windowed, cudaS
   cudaError_t e = cudaErrorNotSupported;
   // few full-window fp32 sectors (one wave of clusters): each spread over a
   // cluster of up to 8 SMs (cluster_kernels.cu)
-  if (!windowed && !rows && kn.cluster && nmax_sector <= 8192)
+  if (!rows) e = run_tiny_any(p, nmax_sector, st);
+  if (e == cudaErrorNotSupported && !windowed && !rows && kn.cluster && nmax_sector <= 8192)
     e = run_cluster_any(p, nmax_sector, st);
   if (e == cudaErrorNotSupported && use_morton &&
       (rows || nmax_sector > morton_min || (busy && morton_tmem)))

@@ -286,5 +286,8 @@ cudaError_t run_morton_any(SampleParams p, long long nmax_sector, cudaStream_t s
 cudaError_t run_morton_tmem_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_stream_any(SampleParams p, long long nmax_sector, cudaStream_t st);
 cudaError_t run_cluster_any(SampleParams p, long long nmax_sector, cudaStream_t st);
+cudaError_t run_tiny_any(SampleParams p, long long nmax_sector, cudaStream_t st);
+// a thread per sector (fps_tiny_kernel) from this many sectors on
+constexpr long long kTinyMinSectors = 2048;
 
 }  // namespace pcsk

@@ -552,6 +552,41 @@ def test_npdu_tmem_high_word_keys_multiwave(reference, n, k, clouds, grid):
     np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
 
 
+@pytest.mark.parametrize("n,m,c", [(2048, 256, 512), (4000, 256, 700), (4096, 256, 1024),
+                                   (1024, 128, 300), (3000, 300, 900)])
+@pytest.mark.parametrize("first", ["fixed", "random"])
+def test_tiny_sectors_thread_per_sector(oracle, n, m, c, first):
+    """>= 2048 sectors of <= 16 points take fps_tiny_kernel (a thread per
+    sector): AFPS and NPDU-AFPS, ragged sector sizes and quotas, coincident
+    points (the all-zero lowest-unsampled path), fp32 and fp64 input, int64
+    indices and sector_of, index / sector bases -- every cloud against the
+    oracle."""
+    import torch
+
+    import paper_2208_08795_b200 as pcs
+    from paper_2208_08795_b200 import sample
+
+    B = max(8, -(-2048 // m))
+    xyz = synth.uniform_cube(B, n, n + m)
+    xyz[1, : n // 2] = xyz[1, 0]                       # coincident points
+    xyz[2] = np.round(xyz[2] * 4) / 4                  # coarse grid: many ties
+    x = torch.from_numpy(xyz).cuda()
+    for meth, k in (("afps", None), ("npdu_afps", 3), ("npdu_afps", 9)):
+        fam = pcs.kernel_family(meth, n, m, k, batch=B, full=True)
+        assert fam.startswith("fps_tiny_kernel"), fam
+        want_idx, want_st = oracle.sample_batch_f32(meth, xyz, c, m, k or 0, first, 5)
+        for xx in (x, x.double()):
+            idx, st, sec = sample(xx, c, method=meth, m=m, k=k, first=first, seed=5,
+                                  index_dtype=torch.int64, return_sector=True)
+            np.testing.assert_array_equal(idx.cpu().numpy(), want_idx, err_msg=f"{meth} {k} {xx.dtype}")
+            np.testing.assert_array_equal(st.cpu().numpy(), want_st.astype(np.int64))
+        for b in (0, 1, B - 1):
+            w_idx, w_sec, _ = oracle.sample(meth, xyz[b].astype(np.float64), c, m, k or 0, first, 5)
+            np.testing.assert_array_equal(sec[b].cpu().numpy(), w_sec)
+        idx, st = sample(x, c, method=meth, m=m, k=k, first=first, seed=5, index_base=1000)
+        np.testing.assert_array_equal(idx.cpu().numpy(), want_idx + 1000)
+
+
 def test_streaming_engine_beyond_on_chip_sectors(oracle):
     """Sectors larger than every on-chip engine (d[] in global memory, one
     cooperative launch per sector, grid barrier per iteration): FPS and NPDU
