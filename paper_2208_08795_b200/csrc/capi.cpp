@@ -310,7 +310,25 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
     // r02 sweep, tools/e2e_parts.py: cfg3 (6.3 MB) 0.288 ms in one chunk vs
     // 0.255 in four, cfg4 (50 MB) best at 8)
     const int64_t by_size = static_cast<int64_t>((cloud_bytes * B) / (size_t(3) << 19));
-    const int64_t def = std::max<int64_t>(1, std::min<int64_t>(8, by_size));
+    int64_t def = std::max<int64_t>(1, std::min<int64_t>(8, by_size));
+    // Compute-heavy calls with few sectors (many reference distance
+    // evaluations per input point, about one wave of sectors: full-window
+    // FPS / AFPS M=1) are bound by their kernels' serial iteration chains,
+    // not by the copy: chunks then only split the batch into launches that
+    // wait on one another (r02,
+    // tools/e2e_parts.py: 256 x 4K FPS 1.86 ms in 4 chunks vs 1.35 in 2,
+    // 256 x 8K 3.64 vs 2.67, 256 x 2K 0.77 vs 0.56 in 1).
+    {
+      const bool windowed = ha->method == PCS_METHOD_NPDU_FPS || ha->method == PCS_METHOD_NPDU_AFPS;
+      const bool sectored = ha->method == PCS_METHOD_AFPS || ha->method == PCS_METHOD_NPDU_AFPS;
+      const int64_t sector = (N + (sectored ? ha->m : 1) - 1) / (sectored ? ha->m : 1);
+      const int64_t per_iter = windowed ? std::min<int64_t>(ha->k, sector) : sector;
+      const double evals_per_point = static_cast<double>(per_iter) * static_cast<double>(C) /
+                                     static_cast<double>(N > 0 ? N : 1);
+      const int64_t sectors = B * (sectored ? ha->m : 1);
+      if (evals_per_point > 256 && sectors <= 2 * 148)
+        def = std::min<int64_t>(def, sector > 2048 ? 2 : 1);
+    }
     const int64_t nu = std::min<int64_t>(std::min<int64_t>(B, chunks > 0 ? chunks : def), kEvents - 4);
     for (int64_t i = 1; i <= nu; ++i) bounds.push_back(B * i / nu);
   }

@@ -50,7 +50,7 @@ def capi(ch):
 
 
 print("h2d_floor", med(h2d))
-for ch in (0, 4, 8, 12, 16, 24, 32):
+for ch in ([int(a) for a in sys.argv[2:]] or (0, 4, 8, 12, 16, 24, 32)):
     print("capi chunks", ch, med(capi(ch)))
 print("wrapper", med(lambda: pcs.sample_host_batch(x, C, method=w["method"], m=w["M"], k=w["K"],
                                                    sort=w["sort"])))
