@@ -718,12 +718,14 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   while (cols < ((G + 3) / 4) * cpw) cols *= 2;
   if (cols > 512) return cudaErrorNotSupported;
   const size_t smem = wsm * G;
-  // key form: multi-wave launches keep every SM's issue slots full, so the
-  // form with the fewest instructions wins (cfg4 0.358 -> 0.355 ms, 256x8K
-  // M=16 0.150 -> 0.144, 256x32K M=16 1.07 -> 0.96); a one-wave launch is
-  // bound by each warp's argmax chain, where the exact index form is the
-  // shortest (cfg3 0.082 vs 0.088 with high-word keys)
-  if (waves >= 2) return launch_npdu_tmem<RMAX, NCAP, kKeyHigh>(p, static_cast<int>(G), cols, smem, st);
+  // key form: launches that keep every SM's issue slots full (two or more
+  // waves, or 16+ sectors per SM) run fastest with the fewest instructions
+  // (cfg4 0.358 -> 0.355 ms, 256x32K M=16 1.07 -> 0.96, 256x8K M=16 0.125 ->
+  // 0.120 one-wave); a launch of a few sectors per SM is bound by each
+  // warp's argmax chain, where the exact index form is the shortest (cfg3,
+  // 7 sectors per SM, 0.082 vs 0.088 ms with high-word keys)
+  if (waves >= 2 || sectors >= 16 * 148)
+    return launch_npdu_tmem<RMAX, NCAP, kKeyHigh>(p, static_cast<int>(G), cols, smem, st);
   if (RMAX >= 5) return launch_npdu_tmem<RMAX, NCAP, kKeyBallot>(p, static_cast<int>(G), cols, smem, st);
   return launch_npdu_tmem<RMAX, NCAP, kKeyIndex>(p, static_cast<int>(G), cols, smem, st);
 }
