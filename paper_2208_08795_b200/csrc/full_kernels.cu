@@ -434,10 +434,10 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   if (n <= 64) return run_full<2, 1, true>(p, st);
   if (n <= 128) return run_full<4, 1, true>(p, st);
   if (n <= 256) {
-    // one sector per SM or fewer: 4 warps x 2 slots shorten the serial chain
-    // (cfg2 0.032 -> 0.027 ms); with many sectors one warp each wins
-    // (AFPS M=16 at 4K: 0.098 vs 0.157 ms)
-    if (p.B * p.M <= 148) return run_full<2, 4, true>(p, st);
+    // one sector per SM or fewer: 8 warps x 1 slot shorten the serial chain
+    // (cfg2 sampler 0.032 -> 0.027 ms with 4 x 2, r02 -> 0.0235 with 8 x 1);
+    // with many sectors one warp each wins (AFPS M=16 at 4K: 0.098 vs 0.157 ms)
+    if (p.B * p.M <= 148) return run_full<1, 8, true>(p, st);
     return run_full<8, 1, true>(p, st);
   }
   // 8 slots per thread (twice the warps, ~120 registers) hides more latency
@@ -450,6 +450,9 @@ cudaError_t run_full_any(SampleParams p, long long n, cudaStream_t st) {
   // 4096 sectors on the 8-slot form wins again, 0.333 vs 0.384 ms at 8K M=16)
   const bool p8 = (sectors >= 4 * 148 && !(n <= 512 && sectors <= 2048)) || sectors <= 148;
   if (p8) {
+    // (at most one sector per SM, 512 points: 8 warps x 2 slots, 16 x 512
+    // AFPS M=4 0.051 -> 0.046 ms; 1024 points keep 4 warps x 8 slots)
+    if (sectors <= 148 && n <= 512) return run_full<2, 8, true>(p, st);
     if (n <= 512) return run_full<8, 2, true>(p, st);
     if (n <= 1024) return run_full<8, 4, true>(p, st);
     if (n <= 2048) return run_full<8, 8, true>(p, st);
