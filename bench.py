@@ -434,7 +434,9 @@ class Runner:
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            # thread_local: other threads' CUDA calls (e.g. the NCCL watchdog
+            # under torchrun) must not invalidate the capture
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 out = fn()
             torch.cuda.synchronize()
             self.graphs.append(g)
@@ -518,7 +520,8 @@ class Runner:
                 total += dt
         e_ms = total * 1e3
         if dist is not None:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=self.dev)
+            red = torch.device("cpu") if dist.get_backend() == "gloo" else self.dev
+            t = torch.tensor([e_ms], dtype=torch.float64, device=red)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e_ms /= steps
@@ -670,10 +673,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PCS_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 over gloo,
+    # to run the torchrun path on a one-GPU box
+    share = os.environ.get("PCS_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if share else dev  # gloo reduces host tensors
     args.warmup = max(args.warmup, 3)
     B, N, C = w["B"], w["N"], w["C"]
 
@@ -710,14 +722,14 @@ def main():
         ms, out = r.timed(step_fn, args.steps)
     if world > 1:
         dist.barrier()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     gpu_idx = out[0].cpu().numpy()
     # the same step launched eagerly from Python (host work between launches)
     eager_ms = r.timed(lambda: r.step(r.xyz), args.steps)[0]
-    t = torch.tensor([eager_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([eager_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     eager_ms = float(t.item()) / args.steps
@@ -734,7 +746,7 @@ def main():
         wfn = rw.graphed(lambda: rw.step(rw.xyz))[0]
         dist.barrier()
         wms = rw.timed(wfn, args.steps)[0]
-        t = torch.tensor([wms], dtype=torch.float64, device=dev)
+        t = torch.tensor([wms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wms = float(t.item()) / args.steps
         weak = {"value": world * B * C / (wms * 1e-3), "unit": "sampled points/s",
