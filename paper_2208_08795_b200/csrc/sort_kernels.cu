@@ -1133,7 +1133,7 @@ __device__ __forceinline__ float key_value(uint32_t k) {
 }
 
 template <int NT, int E, bool KEEP, bool QUAD>
-__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) bucket_sort_kernel(const float* __restrict__ xyz,
+__global__ void __launch_bounds__(NT, NT >= 1024 ? (E <= 2 ? 2 : 1) : 1024 / NT) bucket_sort_kernel(const float* __restrict__ xyz,
                                                              long long N, int axis, int nb, int limit,
                                                              float* __restrict__ out_xyz,
                                                              int* __restrict__ out_perm) {
@@ -1358,13 +1358,15 @@ cudaError_t launch_sort(int coord_dtype, const void* xyz, int64_t batch, int64_t
   // 0.064 vs 0.082, 256 x 32K 0.53 vs 0.63.
   const bool radix_off = !pcs_internal::knobs().sort_radix;
 
-  // at most one cloud per SM of <= 4K points, permutation requested: the
-  // value-bucket sort in 1024-thread CTAs (1-4 keys per thread; a cloud it
-  // cannot bucket falls back to in-CTA all-pairs ranks, no second launch).
-  // r02 perm-only: 16 x 2K 0.0124 -> 0.0103 ms, 148 x 2K 0.0144 -> 0.0103,
-  // 64 x 4K 0.0184 -> 0.0123 (vs radix_reg_kernel)
-  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 4096 && batch <= 148 && out_perm &&
-      pcs_internal::knobs().sort_bucket) {
+  // clouds of 1K-4K points (and <= 148 smaller ones), permutation
+  // requested: the value-bucket sort in 1024-thread CTAs (1-4 keys per
+  // thread, two CTAs per SM up to 2 keys; a cloud it cannot bucket falls
+  // back to in-CTA all-pairs ranks, no second launch). r02 perm-only vs
+  // radix_reg_kernel: 16 x 2K 0.0124 -> 0.0103 ms, 148 x 2K 0.0144 ->
+  // 0.0103, 256 x 2K 0.0184 -> 0.0143, 512 x 2K 0.0246 -> 0.0205, 64 x 4K
+  // 0.0184 -> 0.0123, 256 x 4K 0.0267 -> 0.0205 (256 x 1K equal: radix)
+  if (coord_dtype == PCS_DTYPE_F32 && !radix_off && n <= 4096 && (n > 1024 || batch <= 148) &&
+      out_perm && pcs_internal::knobs().sort_bucket) {
     const float* x = static_cast<const float*>(xyz);
     float* o = static_cast<float*>(out_xyz);
     if (n <= 1024) return pcsk::launch_bucket_sort<1024, 1, true, true>(x, batch, n, axis, o, out_perm, stream);
