@@ -62,6 +62,7 @@ struct Knobs {
   bool sort_bucket = true;    // PCS_SORT_BUCKET=0: 38+ clouds <= 32K take the radix CTA sort
   bool cluster = true;        // PCS_CLUSTER=0: no cluster-spread full-window kernel
   int cluster_cs = 8;         // PCS_CLUSTER_CS: largest cluster it may use (2, 4 or 8)
+  int npdu_key = -1;          // PCS_NPDU_KEY: force the TMEM NPDU row-key form (0-3)
 };
 const Knobs& knobs();
 void reload_knobs();

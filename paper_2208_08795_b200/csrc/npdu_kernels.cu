@@ -395,7 +395,11 @@ __host__ __device__ constexpr size_t tm_warp_smem(int ncap) {
 // keys with an exact slow path. The high-word form issues the fewest
 // instructions (multi-wave launches, which are issue-bound); the exact index
 // form has the shortest argmax chain (one-wave launches, latency-bound).
-enum NpduKey { kKeyIndex = 0, kKeyBallot = 1, kKeyHigh = 2 };
+// kKeyMin: the high-word keys of kKeyHigh plus, per row, the index of the
+// lowest lane holding the row's high word (a redux.sync.min beside the row's
+// ballot), so the sector argmax is max(hi) then min(index) -- two dependent
+// redux.sync, no ballot -> find-first-set -> shuffle -> find-first-set chain.
+enum NpduKey { kKeyIndex = 0, kKeyBallot = 1, kKeyHigh = 2, kKeyMin = 3 };
 
 // fp32 input, sectors <= NCAP <= 4096 points (1-4 cached rows per lane)
 template <int RMAX, int NCAP, int KEY>
@@ -458,12 +462,13 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     //    +inf exactly, all such values are equal, lowest index wins) and
     //    otherwise by an exact slow path that re-reads the candidate rows'
     //    fp64 values from TMEM (measured: 3e-4 of cfg4's iterations).
-    uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL];
+    uint32_t rm_hi[RPL], rm_lo[RPL], rm_m[RPL], rm_j[RPL];
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
       const int r = lane + 32 * i;
       rm_hi[i] = r < rows ? kInfHi : 0u;
       rm_lo[i] = 0u;
+      rm_j[i] = r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex;
       rm_m[i] = KEY == kKeyIndex ? (r < rows ? static_cast<uint32_t>(r * 32) : kNoIndex)
                                  : (r < rows ? 1u : 0u);
     }
@@ -497,169 +502,209 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     };
     int marked = 0;  // outputs [0, marked) are in the bitmap
     unsigned writes = 0;
-    for (int it = 1; it < g.quota; ++it) {
-      const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
-                   pz = static_cast<double>(zs[cur]);
-      const int wb = cur >= half_down ? cur - half_down : 0;
-      const int we = min(n, cur + half_up);
-      // the RMAX rows from r_lo cover the window; near the sector's end
-      // they are shifted down so they stay inside the allocated rows (the
-      // extra rows are masked out and stored back unchanged)
-      const int r_lo = min(wb >> 5, max(rows - RMAX, 0));
-      const int j0 = (r_lo << 5) + lane;
-      // j in [wb, we) <=> (unsigned)(j - wb) < we - wb
-      const uint32_t t0 = static_cast<uint32_t>(j0 - wb), wlen = static_cast<uint32_t>(we - wb);
-      double dj[RMAX], dist[RMAX];
-      tm_wait_st();
-      tm_load_rows<RMAX>(tm + 2 * r_lo, dj);
-#pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
-        // slots past n hold stale shared memory: evaluated, never used
-        const int jc = j0 + 32 * q;
-        dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
-                        static_cast<double>(zs[jc]), px, py, pz);
-      }
-#pragma unroll
-      for (int q = 0; q < RMAX; ++q) {
-        const bool lower = t0 + 32u * q < wlen && dist[q] <= dj[q];
-        writes += lower ? 1u : 0u;
-        dj[q] = lower ? dist[q] : dj[q];
-      }
-      tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
-      uint32_t mh, ml = 0u, j;
-      bool exact;
-      if constexpr (KEY != kKeyHigh) {
+    // blocks of 32 outputs: the inner loop has no flush test
+    for (int blk = 0; blk < g.quota; blk += 32) {
+      const int it_end = min(blk + 32, g.quota);
+#pragma unroll 1
+      for (int it = blk > 0 ? blk : 1; it < it_end; ++it) {
+        const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
+                     pz = static_cast<double>(zs[cur]);
+        const int wb = cur >= half_down ? cur - half_down : 0;
+        const int we = min(n, cur + half_up);
+        // the RMAX rows from r_lo cover the window; near the sector's end
+        // they are shifted down so they stay inside the allocated rows (the
+        // extra rows are masked out and stored back unchanged)
+        const int r_lo = min(wb >> 5, max(rows - RMAX, 0));
+        const int j0 = (r_lo << 5) + lane;
+        // j in [wb, we) <=> (unsigned)(j - wb) < we - wb
+        const uint32_t t0 = static_cast<uint32_t>(j0 - wb), wlen = static_cast<uint32_t>(we - wb);
+        double dj[RMAX], dist[RMAX];
+        tm_wait_st();
+        tm_load_rows<RMAX>(tm + 2 * r_lo, dj);
 #pragma unroll
         for (int q = 0; q < RMAX; ++q) {
-          uint32_t hi, lo, mk;
-          row_key_mask(dj[q], hi, lo, mk);
-          if constexpr (KEY == kKeyIndex) mk = static_cast<uint32_t>(((r_lo + q) << 5) + __ffs(mk) - 1);
-          store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
+          // slots past n hold stale shared memory: evaluated, never used
+          const int jc = j0 + 32 * q;
+          dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
+                          static_cast<double>(zs[jc]), px, py, pz);
         }
-        // this lane's best row (rows grow with i: strict > keeps the lowest),
-        // then the warp's: max d, lowest row among equals, its lowest lane
-        uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
+        unsigned lmask = 0u;
 #pragma unroll
-        for (int i = 1; i < RPL; ++i)
-          if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
-            hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
+        for (int q = 0; q < RMAX; ++q) {
+          const bool lower = t0 + 32u * q < wlen && dist[q] <= dj[q];
+          lmask |= lower ? 1u << q : 0u;
+          dj[q] = lower ? dist[q] : dj[q];
+        }
+        writes += __popc(lmask);
+        tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
+        uint32_t mh, ml = 0u, j;
+        bool exact;
+        if constexpr (KEY == kKeyIndex || KEY == kKeyBallot) {
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q) {
+            uint32_t hi, lo, mk;
+            row_key_mask(dj[q], hi, lo, mk);
+            if constexpr (KEY == kKeyIndex) mk = static_cast<uint32_t>(((r_lo + q) << 5) + __ffs(mk) - 1);
+            store_row<RPL>(r_lo + q, lane, hi, lo, mk, rm_hi, rm_lo, rm_m);
           }
-        j = mk;
-        if constexpr (KEY == kKeyIndex) {
-          warp_argmax(hi, lo, j);
-        } else {
-          const uint32_t wh = __reduce_max_sync(kFull, hi);
-          const uint32_t wl = __reduce_max_sync(kFull, hi == wh ? lo : 0u);
-          const uint32_t mr = __reduce_min_sync(kFull, (hi == wh && lo == wl) ? rsel : kNoIndex);
-          const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
-          hi = wh;
-          lo = wl;
-          j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
-        }
-        mh = hi;
-        ml = lo;
-        exact = (hi | lo) != 0u;
-      } else {
-#pragma unroll
-        for (int q = 0; q < RMAX; ++q) {
-          const uint32_t h = static_cast<uint32_t>(__double2hiint(dj[q]));
-          const uint32_t wk = __reduce_max_sync(kFull, h);
-          const uint32_t mk = __ballot_sync(kFull, h == wk);
-          const int r = r_lo + q;
-#pragma unroll
-          for (int i = 0; i < RPL; ++i)
-            if (r == lane + 32 * i) {
-              rm_hi[i] = wk;
-              rm_m[i] = mk;
-            }
-        }
-        // sector argmax on the high words: max, its lowest row, that row's
-        // lowest lane (rows order indices)
-        uint32_t wm, wr;
-        bool unique;
-        if constexpr (RPL == 1) {
-          mh = __reduce_max_sync(kFull, rm_hi[0]);
-          const uint32_t rb = __ballot_sync(kFull, rm_hi[0] == mh);
-          wr = static_cast<uint32_t>(__ffs(rb)) - 1u;
-          wm = __shfl_sync(kFull, rm_m[0], static_cast<int>(wr));
-          unique = (rb & (rb - 1u)) == 0u;
-        } else {
-          uint32_t lh = rm_hi[0], lm = rm_m[0], ls = static_cast<uint32_t>(lane);
+          // this lane's best row (rows grow with i: strict > keeps the lowest),
+          // then the warp's: max d, lowest row among equals, its lowest lane
+          uint32_t hi = rm_hi[0], lo = rm_lo[0], mk = rm_m[0], rsel = static_cast<uint32_t>(lane);
 #pragma unroll
           for (int i = 1; i < RPL; ++i)
-            if (rm_hi[i] > lh) { lh = rm_hi[i]; lm = rm_m[i]; ls = static_cast<uint32_t>(lane + 32 * i); }
+            if (rm_hi[i] > hi || (rm_hi[i] == hi && rm_lo[i] > lo)) {
+              hi = rm_hi[i]; lo = rm_lo[i]; mk = rm_m[i]; rsel = static_cast<uint32_t>(lane + 32 * i);
+            }
+          j = mk;
+          if constexpr (KEY == kKeyIndex) {
+            warp_argmax(hi, lo, j);
+          } else {
+            const uint32_t wh = __reduce_max_sync(kFull, hi);
+            const uint32_t wl = __reduce_max_sync(kFull, hi == wh ? lo : 0u);
+            const uint32_t mr = __reduce_min_sync(kFull, (hi == wh && lo == wl) ? rsel : kNoIndex);
+            const uint32_t wm = __shfl_sync(kFull, mk, static_cast<int>(mr & 31u));
+            hi = wh;
+            lo = wl;
+            j = (mr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+          }
+          mh = hi;
+          ml = lo;
+          exact = (hi | lo) != 0u;
+        } else if constexpr (KEY == kKeyMin) {
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q) {
+            const uint32_t h = static_cast<uint32_t>(__double2hiint(dj[q]));
+            const uint32_t wk = __reduce_max_sync(kFull, h);
+            const bool eq = h == wk;
+            const uint32_t ll = __reduce_min_sync(kFull, eq ? static_cast<uint32_t>(lane) : 32u);
+            const uint32_t mk = __ballot_sync(kFull, eq);
+            const int r = r_lo + q;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i)
+              if (r == lane + 32 * i) {
+                rm_hi[i] = wk;
+                rm_j[i] = (static_cast<uint32_t>(r) << 5) + ll;
+                rm_m[i] = mk;
+              }
+          }
+          // this lane's best row (max high word, lowest row), then the
+          // sector's: max high word, lowest index among the rows holding it.
+          // Exact unless a high-word tie is possible: two candidate rows, or a
+          // candidate row whose high word two lanes share (+inf ties are exact)
+          uint32_t lh = rm_hi[0], lj = rm_j[0], lm = rm_m[0];
+#pragma unroll
+          for (int i = 1; i < RPL; ++i)
+            if (rm_hi[i] > lh) { lh = rm_hi[i]; lj = rm_j[i]; lm = rm_m[i]; }
           int dup = 0;
 #pragma unroll
           for (int i = 0; i < RPL; ++i) dup += rm_hi[i] == lh ? 1 : 0;
           mh = __reduce_max_sync(kFull, lh);
-          const uint32_t rb = __ballot_sync(kFull, lh == mh);
-          const uint32_t rd = __ballot_sync(kFull, lh == mh && dup > 1);
-          wr = __reduce_min_sync(kFull, lh == mh ? ls : kNoIndex);
-          wm = __shfl_sync(kFull, lm, static_cast<int>(wr & 31u));
-          unique = (rb & (rb - 1u)) == 0u && rd == 0u;
-        }
-        j = (wr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
-        exact = mh == kInfHi || (mh != 0u && unique && (wm & (wm - 1u)) == 0u);
-      }
-      if (!exact) {
-        uint32_t bh = mh, bl = ml;
-        if constexpr (KEY == kKeyHigh) {
-          // exact resolution over the candidate rows (a high-word tie, or
-          // every cached key 0): (max d, lowest index) from the fp64 values
-          tm_wait_st();
-          bh = bl = 0u;
-          j = kNoIndex;
+          const bool cand = lh == mh;
+          j = __reduce_min_sync(kFull, cand ? lj : kNoIndex);
+          const uint32_t rb = __ballot_sync(kFull, cand);
+          const uint32_t bad = __ballot_sync(kFull, cand && (dup > 1 || (lm & (lm - 1u)) != 0u));
+          exact = mh == kInfHi || (mh != 0u && (rb & (rb - 1u)) == 0u && bad == 0u);
+        } else {
 #pragma unroll
-          for (int i = 0; i < RPL; ++i) {
-            uint32_t cand = __ballot_sync(kFull, rm_hi[i] == mh && lane + 32 * i < rows);
-            while (cand) {
-              const int r = __ffs(cand) - 1 + 32 * i;
-              cand &= cand - 1u;
-              uint32_t t[2];
-              tm_ld(tm + 2 * r, t);
-              tm_wait_ld();
-              uint32_t h, l, mk;
-              // pad lanes past n hold d = 0 and are never written
-              row_key_mask(__hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0])), h, l, mk);
-              if (h > bh || (h == bh && l > bl) || j == kNoIndex) {
-                bh = h;
-                bl = l;
-                j = static_cast<uint32_t>((r << 5) + __ffs(mk) - 1);
+          for (int q = 0; q < RMAX; ++q) {
+            const uint32_t h = static_cast<uint32_t>(__double2hiint(dj[q]));
+            const uint32_t wk = __reduce_max_sync(kFull, h);
+            const uint32_t mk = __ballot_sync(kFull, h == wk);
+            const int r = r_lo + q;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i)
+              if (r == lane + 32 * i) {
+                rm_hi[i] = wk;
+                rm_m[i] = mk;
+              }
+          }
+          // sector argmax on the high words: max, its lowest row, that row's
+          // lowest lane (rows order indices)
+          uint32_t wm, wr;
+          bool unique;
+          if constexpr (RPL == 1) {
+            mh = __reduce_max_sync(kFull, rm_hi[0]);
+            const uint32_t rb = __ballot_sync(kFull, rm_hi[0] == mh);
+            wr = static_cast<uint32_t>(__ffs(rb)) - 1u;
+            wm = __shfl_sync(kFull, rm_m[0], static_cast<int>(wr));
+            unique = (rb & (rb - 1u)) == 0u;
+          } else {
+            uint32_t lh = rm_hi[0], lm = rm_m[0], ls = static_cast<uint32_t>(lane);
+#pragma unroll
+            for (int i = 1; i < RPL; ++i)
+              if (rm_hi[i] > lh) { lh = rm_hi[i]; lm = rm_m[i]; ls = static_cast<uint32_t>(lane + 32 * i); }
+            int dup = 0;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) dup += rm_hi[i] == lh ? 1 : 0;
+            mh = __reduce_max_sync(kFull, lh);
+            const uint32_t rb = __ballot_sync(kFull, lh == mh);
+            const uint32_t rd = __ballot_sync(kFull, lh == mh && dup > 1);
+            wr = __reduce_min_sync(kFull, lh == mh ? ls : kNoIndex);
+            wm = __shfl_sync(kFull, lm, static_cast<int>(wr & 31u));
+            unique = (rb & (rb - 1u)) == 0u && rd == 0u;
+          }
+          j = (wr << 5) + static_cast<uint32_t>(__ffs(wm)) - 1u;
+          exact = mh == kInfHi || (mh != 0u && unique && (wm & (wm - 1u)) == 0u);
+        }
+        if (!exact) {
+          uint32_t bh = mh, bl = ml;
+          if constexpr (KEY == kKeyHigh || KEY == kKeyMin) {
+            // exact resolution over the candidate rows (a high-word tie, or
+            // every cached key 0): (max d, lowest index) from the fp64 values
+            tm_wait_st();
+            bh = bl = 0u;
+            j = kNoIndex;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              uint32_t cand = __ballot_sync(kFull, rm_hi[i] == mh && lane + 32 * i < rows);
+              while (cand) {
+                const int r = __ffs(cand) - 1 + 32 * i;
+                cand &= cand - 1u;
+                uint32_t t[2];
+                tm_ld(tm + 2 * r, t);
+                tm_wait_ld();
+                uint32_t h, l, mk;
+                // pad lanes past n hold d = 0 and are never written
+                row_key_mask(__hiloint2double(static_cast<int>(t[1]), static_cast<int>(t[0])), h, l, mk);
+                if (h > bh || (h == bh && l > bl) || j == kNoIndex) {
+                  bh = h;
+                  bl = l;
+                  j = static_cast<uint32_t>((r << 5) + __ffs(mk) - 1);
+                }
               }
             }
           }
-        }
-        if ((bh | bl) == 0u) {
-          // every distance is 0: lowest unsampled index (sampler.cpp:148-154);
-          // fold outputs [marked, it) into the bitmap: whole blocks from
-          // global memory, the current block from the lanes' buffers
-          const int t_blk = (it - 1) & ~31;
-          __syncwarp();
-          for (int t = marked + lane; t < t_blk; t += 32) {
-            const long long v = idx64 ? out64[t] : static_cast<long long>(out32[t]);
-            const int jl = static_cast<int>(v - index_off);
-            atomicOr(&sampled[jl >> 5], 1u << (jl & 31));
-          }
-          if (lane <= ((it - 1) & 31) && t_blk + lane >= marked)
-            atomicOr(&sampled[ob >> 5], 1u << (ob & 31));
-          marked = it;
-          __syncwarp();
-          uint32_t jm = kNoIndex;
-          for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
-            const unsigned free_bits = ~sampled[w];
-            if (free_bits) {
-              const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
-              if (cand < static_cast<uint32_t>(n)) jm = cand;
+          if ((bh | bl) == 0u) {
+            // every distance is 0: lowest unsampled index (sampler.cpp:148-154);
+            // fold outputs [marked, it) into the bitmap: whole blocks from
+            // global memory, the current block from the lanes' buffers
+            const int t_blk = (it - 1) & ~31;
+            __syncwarp();
+            for (int t = marked + lane; t < t_blk; t += 32) {
+              const long long v = idx64 ? out64[t] : static_cast<long long>(out32[t]);
+              const int jl = static_cast<int>(v - index_off);
+              atomicOr(&sampled[jl >> 5], 1u << (jl & 31));
             }
+            if (lane <= ((it - 1) & 31) && t_blk + lane >= marked)
+              atomicOr(&sampled[ob >> 5], 1u << (ob & 31));
+            marked = it;
+            __syncwarp();
+            uint32_t jm = kNoIndex;
+            for (int w = lane; w < rows && jm == kNoIndex; w += 32) {
+              const unsigned free_bits = ~sampled[w];
+              if (free_bits) {
+                const uint32_t cand = static_cast<uint32_t>(w * 32 + __ffs(free_bits) - 1);
+                if (cand < static_cast<uint32_t>(n)) jm = cand;
+              }
+            }
+            j = __reduce_min_sync(kFull, jm);
           }
-          j = __reduce_min_sync(kFull, jm);
         }
+        cur = static_cast<int>(j);
+        ob = lane == (it & 31) ? cur : ob;
       }
-      cur = static_cast<int>(j);
-      if (lane == (it & 31)) ob = cur;
-      if ((it & 31) == 31) flush(it - 31, 32);
+      flush(blk, it_end - blk);
     }
-    if (((g.quota - 1) & 31) != 31) flush((g.quota - 1) & ~31, ((g.quota - 1) & 31) + 1);
     tm_wait_st();
     const unsigned ws = __reduce_add_sync(kFull, writes);
     // per-lane window sums (< 2^32 each: a lane holds <= quota/32 outputs
@@ -719,13 +764,24 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
   if (cols > 512) return cudaErrorNotSupported;
   const size_t smem = wsm * G;
   // key form: launches that keep every SM's issue slots full (two or more
-  // waves, or 16+ sectors per SM) run fastest with the fewest instructions
-  // (cfg4 0.358 -> 0.355 ms, 256x32K M=16 1.07 -> 0.96, 256x8K M=16 0.125 ->
-  // 0.120 one-wave); a launch of a few sectors per SM is bound by each
-  // warp's argmax chain, where the exact index form is the shortest (cfg3,
-  // 7 sectors per SM, 0.082 vs 0.088 ms with high-word keys)
+  // waves, or 16+ sectors per SM) take the high-word keys (few instructions
+  // per touched row: cfg4 0.358 -> 0.355 ms, 256x32K M=16 1.07 -> 0.96),
+  // with the per-row lowest-lane indices (kKeyMin: the sector argmax is two
+  // dependent redux.sync instead of a redux -> ballot -> ffs -> shfl -> ffs
+  // chain; r02 s3 A/B vs kKeyHigh: 256x16K M=16 0.333 -> 0.310 ms, 256x32K
+  // 0.962 -> 0.920, cfg4 0.355 -> 0.351; profiles/r02_npdu_keymin_ab.log); a
+  // launch of a few sectors per SM is bound by each warp's argmax chain,
+  // where the exact index form is the shortest (cfg3, 7 sectors per SM,
+  // 0.082 vs 0.088 ms with high-word keys). PCS_NPDU_KEY forces a form.
+  switch (pcs_internal::knobs().npdu_key) {
+    case kKeyIndex: return launch_npdu_tmem<RMAX, NCAP, kKeyIndex>(p, static_cast<int>(G), cols, smem, st);
+    case kKeyBallot: return launch_npdu_tmem<RMAX, NCAP, kKeyBallot>(p, static_cast<int>(G), cols, smem, st);
+    case kKeyHigh: return launch_npdu_tmem<RMAX, NCAP, kKeyHigh>(p, static_cast<int>(G), cols, smem, st);
+    case kKeyMin: return launch_npdu_tmem<RMAX, NCAP, kKeyMin>(p, static_cast<int>(G), cols, smem, st);
+    default: break;
+  }
   if (waves >= 2 || sectors >= 16 * 148)
-    return launch_npdu_tmem<RMAX, NCAP, kKeyHigh>(p, static_cast<int>(G), cols, smem, st);
+    return launch_npdu_tmem<RMAX, NCAP, kKeyMin>(p, static_cast<int>(G), cols, smem, st);
   if (RMAX >= 5) return launch_npdu_tmem<RMAX, NCAP, kKeyBallot>(p, static_cast<int>(G), cols, smem, st);
   return launch_npdu_tmem<RMAX, NCAP, kKeyIndex>(p, static_cast<int>(G), cols, smem, st);
 }

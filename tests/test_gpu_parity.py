@@ -524,21 +524,24 @@ def test_npdu_tmem_high_word_ties(oracle, monkeypatch, grid):
 
 @pytest.mark.parametrize("n,k,clouds", [(256, 65, 150), (2048, 65, 170), (4096, 129, 150)])
 @pytest.mark.parametrize("grid", [0, 8, 1 << 20])
-def test_npdu_tmem_high_word_keys_multiwave(reference, n, k, clouds, grid):
-    """Multi-wave TMEM NPDU launches take the high-word row keys
-    (npdu_tmem_kernel<R,NCAP,2>, 1, 2 and 4 cached rows per lane) -- under
-    ties: coarse grids (equal distances), distances a few ulps apart (high
-    words tie, low words differ) and uniform coordinates; every cloud
+@pytest.mark.parametrize("key", [None, "2"])
+def test_npdu_tmem_high_word_keys_multiwave(reference, monkeypatch, n, k, clouds, grid, key):
+    """Multi-wave TMEM NPDU launches take the high-word row keys with
+    per-row lowest-lane indices (npdu_tmem_kernel<R,NCAP,3>; key "2": the
+    high-word keys with the ballot argmax), 1, 2 and 4 cached rows per lane
+    -- under ties: coarse grids (equal distances), distances a few ulps apart
+    (high words tie, low words differ) and uniform coordinates; every cloud
     against the reference."""
     import torch
 
     import paper_2208_08795_b200 as pcs
     from paper_2208_08795_b200 import sample
 
+    setknob(monkeypatch, "PCS_NPDU_KEY", key)
     m = 32
     N, c = n * m, n * m // 4
     fam = pcs.kernel_family("npdu_afps", N, m, k, batch=clouds, full=True)
-    assert fam.startswith("npdu_tmem_kernel<") and fam.endswith(",2>"), fam
+    assert fam.startswith("npdu_tmem_kernel<") and fam.endswith(f",{key or 3}>"), fam
     rng = np.random.default_rng(grid + n)
     xyz = synth.uniform_cube(clouds, N, n + grid)
     if grid == 8:

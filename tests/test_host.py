@@ -256,7 +256,7 @@ def test_kernel_family_is_the_dispatch_decision(pcs, monkeypatch):
     assert kf("npdu_fps", 8192, 1, 65, batch=1) == "morton_tmem_kernel"        # > 4096 points
     assert kf("afps", 2048, 8, batch=16) == "fps_full_kernel"                  # cfg2
     assert kf("fps", 8192, 1, batch=64) == "morton_tmem_kernel"                # cfg3 FPS
-    assert kf("npdu_afps", 32768, 32, 129, batch=128, full=True) == "npdu_tmem_kernel<5,1024,2>"
+    assert kf("npdu_afps", 32768, 32, 129, batch=128, full=True) == "npdu_tmem_kernel<5,1024,3>"
     assert kf("npdu_afps", 32768, 32, 129, batch=16, full=True) == "npdu_tmem_kernel<5,1024,1>"
     assert kf("npdu_afps", 8192, 16, 65, batch=64, full=True) == "npdu_tmem_kernel<3,512,0>"
     assert kf("fps", 1 << 20) == "stream_sector_kernel"
