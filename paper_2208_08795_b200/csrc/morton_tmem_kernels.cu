@@ -49,6 +49,12 @@ __host__ __device__ __forceinline__ int morton_cell_bits(int np) {
   return b;
 }
 
+// four-row update steps for 4-warp CTAs with 3+ candidate rows (A/B: -DMORTON_QUAD=0)
+#ifndef MORTON_QUAD
+#define MORTON_QUAD 1
+#endif
+constexpr bool kQuadRows = MORTON_QUAD != 0;
+
 __device__ __forceinline__ void tm_row_ld(uint32_t a, double& d, uint32_t& orig) {
   uint32_t r[4];
   tm_ld(a, r);
@@ -310,44 +316,62 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
     pacc[4] += __popc(todo);
 #endif
     tm_wait_st();  // last iteration's row stores land before rows are re-read
+    // candidate rows, NR per step (independent distance chains overlap).
+    // 4-warp CTAs (many rows per warp) take 3+ candidates four at a time
+    // (AFPS M=16 at 32K 2.98 -> 2.92 ms, M=4 at 8K 1.094 -> 1.067); with 8 or
+    // 16 warps the four-row step measured 3-7% slower
+    // (profiles/r02_morton_quad_ab.log). Missing rows repeat the first one
+    // and store its final value again
+    auto update_rows = [&](auto nr_tag) {
+      constexpr int NR = decltype(nr_tag)::value;
+      int l[NR];
+      l[0] = __ffs(todo) - 1;
+      todo &= todo - 1;
+#pragma unroll
+      for (int q = 1; q < NR; ++q) {
+        l[q] = todo ? __ffs(todo) - 1 : l[0];
+        todo &= todo - 1;
+      }
+      uint32_t r4[NR][4];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) tm_ld(tm + 4 * l[q], r4[q]);
+      double e[NR];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int j = ((warp + W * l[q]) << 5) + lane;
+        e[q] = dist2(to_f64<F2F>(xs[j]), to_f64<F2F>(ys[j]), to_f64<F2F>(zs[j]), px, py, pz);
+      }
+      tm_wait_ld();
+      double d[NR];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        d[q] = __hiloint2double(static_cast<int>(r4[q][1]), static_cast<int>(r4[q][0]));
+        bool w = (q == 0 || l[q] != l[0]) && r4[q][2] != kNoIndex && e[q] <= d[q];
+        if constexpr (WIN)
+          w = w && static_cast<int>(r4[q][2]) >= wb && static_cast<int>(r4[q][2]) < we;
+        writes += w ? 1u : 0u;
+        d[q] = w ? e[q] : d[q];
+      }
+#pragma unroll
+      for (int q = 1; q < NR; ++q) d[q] = l[q] == l[0] ? d[0] : d[q];
+      uint32_t h[NR];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const uint32_t sd[2] = {static_cast<uint32_t>(__double2loint(d[q])),
+                                static_cast<uint32_t>(__double2hiint(d[q]))};
+        tm_st(tm + 4 * l[q], sd);
+        h[q] = __reduce_max_sync(kFull, sd[1]);
+      }
+#pragma unroll
+      for (int q = NR - 1; q >= 0; --q)
+        if (lane == l[q]) rmh = h[q];
+    };
     while (todo) {
 #ifdef PCS_PROF
       pacc[5] += 1;
 #endif
-      const int la = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int lb2 = todo ? __ffs(todo) - 1 : la;
-      todo &= todo - 1;
-      const int ja = ((warp + W * la) << 5) + lane, jb = ((warp + W * lb2) << 5) + lane;
-      uint32_t ra4[4], rb4[4];
-      tm_ld(tm + 4 * la, ra4);
-      tm_ld(tm + 4 * lb2, rb4);
-      const double ea = dist2(to_f64<F2F>(xs[ja]), to_f64<F2F>(ys[ja]), to_f64<F2F>(zs[ja]),
-                              px, py, pz);
-      const double eb = dist2(to_f64<F2F>(xs[jb]), to_f64<F2F>(ys[jb]), to_f64<F2F>(zs[jb]),
-                              px, py, pz);
-      tm_wait_ld();
-      double da = __hiloint2double(static_cast<int>(ra4[1]), static_cast<int>(ra4[0]));
-      double db = __hiloint2double(static_cast<int>(rb4[1]), static_cast<int>(rb4[0]));
-      bool wa = ra4[2] != kNoIndex && ea <= da;
-      bool wbb = lb2 != la && rb4[2] != kNoIndex && eb <= db;
-      if constexpr (WIN) {
-        wa = wa && static_cast<int>(ra4[2]) >= wb && static_cast<int>(ra4[2]) < we;
-        wbb = wbb && static_cast<int>(rb4[2]) >= wb && static_cast<int>(rb4[2]) < we;
-      }
-      writes += (wa ? 1u : 0u) + (wbb ? 1u : 0u);
-      da = wa ? ea : da;
-      db = lb2 == la ? da : (wbb ? eb : db);
-      const uint32_t sa[2] = {static_cast<uint32_t>(__double2loint(da)),
-                              static_cast<uint32_t>(__double2hiint(da))};
-      const uint32_t sb[2] = {static_cast<uint32_t>(__double2loint(db)),
-                              static_cast<uint32_t>(__double2hiint(db))};
-      tm_st(tm + 4 * la, sa);
-      tm_st(tm + 4 * lb2, sb);
-      const uint32_t ha = __reduce_max_sync(kFull, sa[1]);
-      const uint32_t hb = __reduce_max_sync(kFull, sb[1]);
-      if (lane == lb2) rmh = hb;
-      if (lane == la) rmh = ha;
+      if (kQuadRows && W == 4 && __popc(todo) > 2) update_rows(std::integral_constant<int, 4>{});
+      else update_rows(std::integral_constant<int, 2>{});
     }
     tm_wait_st();
     TPROF_T(t1);
