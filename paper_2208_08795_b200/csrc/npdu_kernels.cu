@@ -402,8 +402,15 @@ __host__ __device__ constexpr size_t tm_warp_smem(int ncap) {
 enum NpduKey { kKeyIndex = 0, kKeyBallot = 1, kKeyHigh = 2, kKeyMin = 3 };
 
 // fp32 input, sectors <= NCAP <= 4096 points (1-4 cached rows per lane)
-template <int RMAX, int NCAP, int KEY>
-__global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
+// MAXT: the CTA width the launch uses at most. The register budget follows
+// it: the 4-warp CTAs of multi-wave launches (16 warps per SM) and CTAs of up
+// to 16 warps get up to 128 registers per thread instead of the 64 a
+// 1024-thread bound allows -- the 64-register build rematerialised addresses
+// and window terms every iteration (r02 s4, eager launches: cfg4 0.361 ->
+// 0.306 ms, 256x32K M=16 0.96 -> 0.86, 256x16K 0.312 -> 0.288;
+// profiles/r02_npdu_launch_bounds_ab.log)
+template <int RMAX, int NCAP, int KEY, int MAXT = 1024>
+__global__ void __launch_bounds__(MAXT, MAXT == 128 ? 4 : 1) npdu_tmem_kernel(const SampleParams p, int tm_cols) {
   static_assert(NCAP >= 32 * RMAX && NCAP <= 4096, "capacity");
   constexpr int RPL = NCAP > 1024 ? NCAP / 1024 : 1;  // rows per lane (row r: lane r % 32)
   extern __shared__ __align__(16) unsigned char smem[];
@@ -603,7 +610,8 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
           j = __reduce_min_sync(kFull, cand ? lj : kNoIndex);
           const uint32_t rb = __ballot_sync(kFull, cand);
           const uint32_t bad = __ballot_sync(kFull, cand && (dup > 1 || (lm & (lm - 1u)) != 0u));
-          exact = mh == kInfHi || (mh != 0u && (rb & (rb - 1u)) == 0u && bad == 0u);
+          // (bitwise: one predicate and one branch on the fast path)
+          exact = (mh == kInfHi) | ((mh != 0u) & ((rb & (rb - 1u)) == 0u) & (bad == 0u));
         } else {
 #pragma unroll
           for (int q = 0; q < RMAX; ++q) {
@@ -725,10 +733,10 @@ __global__ void __launch_bounds__(1024) npdu_tmem_kernel(const SampleParams p, i
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tm_base), "r"(tm_cols));
 }
 
-template <int RMAX, int NCAP, int KEY>
+template <int RMAX, int NCAP, int KEY, int MAXT = 1024>
 cudaError_t launch_npdu_tmem(SampleParams p, int G, int cols, size_t smem, cudaStream_t st) {
   if (plan("npdu_tmem_kernel", {RMAX, NCAP, KEY})) return cudaSuccess;
-  auto kern = npdu_tmem_kernel<RMAX, NCAP, KEY>;
+  auto kern = npdu_tmem_kernel<RMAX, NCAP, KEY, MAXT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -780,10 +788,15 @@ cudaError_t run_npdu_tmem(SampleParams p, cudaStream_t st) {
     case kKeyMin: return launch_npdu_tmem<RMAX, NCAP, kKeyMin>(p, static_cast<int>(G), cols, smem, st);
     default: break;
   }
-  if (waves >= 2 || sectors >= 16 * 148)
-    return launch_npdu_tmem<RMAX, NCAP, kKeyMin>(p, static_cast<int>(G), cols, smem, st);
-  if (RMAX >= 5) return launch_npdu_tmem<RMAX, NCAP, kKeyBallot>(p, static_cast<int>(G), cols, smem, st);
-  return launch_npdu_tmem<RMAX, NCAP, kKeyIndex>(p, static_cast<int>(G), cols, smem, st);
+  const int g = static_cast<int>(G);
+  if (G == 4 && waves >= 2) return launch_npdu_tmem<RMAX, NCAP, kKeyMin, 128>(p, 4, cols, smem, st);
+  if (waves >= 2 || sectors >= 16 * 148) {
+    if (G <= 16) return launch_npdu_tmem<RMAX, NCAP, kKeyMin, 512>(p, g, cols, smem, st);
+    return launch_npdu_tmem<RMAX, NCAP, kKeyMin>(p, g, cols, smem, st);
+  }
+  constexpr int kOneWave = RMAX >= 5 ? kKeyBallot : kKeyIndex;
+  if (G <= 16) return launch_npdu_tmem<RMAX, NCAP, kOneWave, 512>(p, g, cols, smem, st);
+  return launch_npdu_tmem<RMAX, NCAP, kOneWave>(p, g, cols, smem, st);
 }
 
 cudaError_t run_npdu_any(SampleParams p, long long n, cudaStream_t st) {
