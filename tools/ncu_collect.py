@@ -10,7 +10,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
-sweep = {}
+# merge into the committed sweep (a partial re-run refreshes its workloads only)
+_prev = os.path.join(ROOT, "profiles", "r02_ncu_sweep.json")
+sweep = json.load(open(_prev)) if os.path.exists(_prev) else {}
 for path in sorted(glob.glob(os.path.join(src, "ncu2_*_*.json"))):
     m = re.match(r"ncu2_(.+)_(sampler|sort)\.json$", os.path.basename(path))
     try:
