@@ -12,6 +12,24 @@ __device__ unsigned long long g_fprof[8];
 
 namespace pcsk {
 
+// A/B switch of the slot loop's hand-spelled update + argmax step
+#ifndef PCS_FULL_ASM
+#define PCS_FULL_ASM 1
+#endif
+constexpr bool kSlotAsm = PCS_FULL_ASM != 0;
+#ifndef PCS_FULL_CHAIN
+#define PCS_FULL_CHAIN 4
+#endif
+constexpr int kChainLen = PCS_FULL_CHAIN;
+
+// (best, bs) <- (bits, k) when bits > best: one 64-bit compare, three selects
+__device__ __forceinline__ void argmax_step(unsigned long long& best, int& bs,
+                                            unsigned long long bits, int k) {
+  asm("{\n .reg .pred p;\n setp.gt.u64 p, %2, %0;\n selp.b64 %0, %2, %0, p;\n"
+      " selp.b32 %1, %3, %1, p;\n}"
+      : "+l"(best), "+r"(bs) : "l"(bits), "r"(k));
+}
+
 // ---------------------------------------------------------------- full window
 // FPS / AFPS: every iteration updates the whole sector (sampler.cpp:115-129
 // with window == sector). REGC: sector xyz also cached in registers.
@@ -72,8 +90,20 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
   for (int it = 1; it < gs.g.quota; ++it) {
     FPROF_T(t0);
     const double px = gs.xs[cur], py = gs.ys[cur], pz = gs.zs[cur];
-    unsigned long long best = 0;
-    int bs = -1;
+    // The update + running-argmax step of a slot, hand-spelled for 4 and 8
+    // slots per thread (r02 s4, profiles/r02_full_slot_asm_ab.log: AFPS M=16
+    // at 16K 1.31 -> 1.19 ms, M=64 at 32K 1.28 -> 1.20, M=16 at 8K 0.358 ->
+    // 0.337; with 16 slots the compiler's own schedule is 20% faster, with 1-2
+    // there is nothing to gain)
+    constexpr bool kAsm = REGC && kSlotAsm && (P == 4 || P == 8);
+    // (hand-spelled form: the running argmax as kChains independent chains
+    // over contiguous slot blocks, merged in slot order with the same strict
+    // compare, so the lowest slot still wins a tie)
+    constexpr int kChains = (kAsm && P > kChainLen) ? P / kChainLen : 1;
+    unsigned long long bestc[kChains];
+    int bsc[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) { bestc[c] = 0; bsc[c] = -1; }
     // Branch-free over the slots so independent slots interleave (ILP).
     // Padding slots (j >= n) hold d = 0 and NaN coordinates (REGC): they
     // never win the argmax (best starts at 0 with a strict >) and never
@@ -85,15 +115,33 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
       const double yy = REGC ? y[REGC ? k : 0] : gs.ys[min(j, n - 1)];
       const double zz = REGC ? z[REGC ? k : 0] : gs.zs[min(j, n - 1)];
       const double dist = dist2(xx, yy, zz, px, py, pz);
-      const bool lower = dist <= d[k];
-      writes += (lower && (REGC || ((vmask >> k) & 1u))) ? 1u : 0u;
-      d[k] = lower ? dist : d[k];
-      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
-      if (bits > best) {
-        best = bits;
-        bs = k;
+      if constexpr (kAsm) {
+        // one predicate per step, spelled out: the compiler's own form of
+        // this loop re-derives the comparisons for the slot index (4 ISETP +
+        // 3 SEL per slot) and counts writes with an add and a move
+        // (profiles/r02_full_slot_asm_ab.log)
+        asm("{\n .reg .pred p;\n setp.le.f64 p, %2, %1;\n selp.f64 %1, %2, %1, p;\n"
+            " @p add.u32 %0, %0, 1;\n}"
+            : "+r"(writes), "+d"(d[k]) : "d"(dist));
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+        argmax_step(bestc[k * kChains / P], bsc[k * kChains / P], bits, k);
+      } else {
+        unsigned long long& best = bestc[0];
+        int& bs = bsc[0];
+        const bool lower = dist <= d[k];
+        writes += (lower && (REGC || ((vmask >> k) & 1u))) ? 1u : 0u;
+        d[k] = lower ? dist : d[k];
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+        if (bits > best) {
+          best = bits;
+          bs = k;
+        }
       }
     }
+#pragma unroll
+    for (int c = 1; c < kChains; ++c) argmax_step(bestc[0], bsc[0], bestc[c], bsc[c]);
+    const unsigned long long best = bestc[0];
+    const int bs = bsc[0];
     if (trace) {
 #pragma unroll
       for (int k = 0; k < P; ++k)
