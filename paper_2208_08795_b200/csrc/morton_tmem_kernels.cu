@@ -55,6 +55,7 @@ __host__ __device__ __forceinline__ int morton_cell_bits(int np) {
 #endif
 constexpr bool kQuadRows = MORTON_QUAD != 0;
 
+
 __device__ __forceinline__ void tm_row_ld(uint32_t a, double& d, uint32_t& orig) {
   uint32_t r[4];
   tm_ld(a, r);
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
   __shared__ uint32_t tm_base_sh;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int T = W * 32;
+  const bool dense = gridDim.x >= 148u;  // a CTA or more per SM
   const int rank = CS > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   const long long flat = static_cast<long long>(blockIdx.x) / CS;
   const long long b = flat / p.M, s = flat % p.M;
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
 #ifdef PCS_PROF
       pacc[5] += 1;
 #endif
-      if (kQuadRows && W == 4 && __popc(todo) > 2) update_rows(std::integral_constant<int, 4>{});
+      if (kQuadRows && (W == 4 || (W == 8 && dense)) && __popc(todo) > 2) update_rows(std::integral_constant<int, 4>{});
       else update_rows(std::integral_constant<int, 2>{});
     }
     tm_wait_st();
@@ -494,7 +496,14 @@ __global__ void __launch_bounds__(W * 32) morton_tmem_kernel(const SampleParams 
 #endif
   }
   };
-  if (any_sub)
+  // fp32 -> fp64 of the candidate rows' coordinates: F2F (XU pipe; always
+  // exact) or integer widening (exact without subnormals). r02 s4 A/B
+  // (profiles/r02_morton_f2f_ab.log): F2F is faster in 16-warp CTAs (FPS 16K
+  // 6.94 -> 6.38 ms, 32K 34.7 -> 31.8) and in 4-warp CTAs (AFPS M=16 at 32K
+  // 2.91 -> 2.49); 8-warp CTAs take it, with four-row steps, when every SM
+  // has a CTA (`dense`: FPS 8K 2.11 -> 2.02, 4K 1.06 -> 1.03) and keep the
+  // integer form and row pairs below that (cfg3 FPS, 64 CTAs: 1.49 vs 1.53)
+  if (any_sub || W != 8 || dense)
     iterate(std::true_type{});
   else
     iterate(std::false_type{});
