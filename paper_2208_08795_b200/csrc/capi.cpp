@@ -63,6 +63,7 @@ Knobs read_knobs() {
   if (const char* v = env("PCS_NPDU_WIDE")) k.npdu_wide = std::atoll(v);
   if (const char* v = env("PCS_NPDU_TMEM")) k.npdu_tmem = v[0] != '0';
   if (const char* v = env("PCS_NPDU_KEY")) k.npdu_key = std::atoi(v);
+  if (const char* v = env("PCS_MORTON_W")) k.morton_w = std::atoi(v);
   if (const char* v = env("PCS_TINY")) k.tiny = v[0] != '0';
   if (const char* v = env("PCS_NPDU_BIG")) k.npdu_big = v[0] != '0';
   if (const char* v = env("PCS_SORT_RADIX")) k.sort_radix = v[0] != '0';

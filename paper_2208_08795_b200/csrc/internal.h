@@ -63,6 +63,7 @@ struct Knobs {
   bool cluster = true;        // PCS_CLUSTER=0: no cluster-spread full-window kernel
   int cluster_cs = 8;         // PCS_CLUSTER_CS: largest cluster it may use (2, 4 or 8)
   int npdu_key = -1;          // PCS_NPDU_KEY: force the TMEM NPDU row-key form (0-3)
+  int morton_w = 0;           // PCS_MORTON_W: force the TMEM Morton engine's warps per CTA (4, 8, 16)
 };
 const Knobs& knobs();
 void reload_knobs();

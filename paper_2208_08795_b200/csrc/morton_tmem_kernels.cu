@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "internal.h"
 #include "rows_common.cuh"
 #include "tmem.cuh"
 
@@ -582,6 +583,8 @@ cudaError_t launch_morton_tmem(SampleParams p, int rows, cudaStream_t st) {
 // (r01: 256 x 4K FPS 1.24 -> 1.13 ms; with ~7 sectors per SM the smaller
 // CTAs win: AFPS M=4 at 8K 1.09 vs 1.37 ms).
 int morton_tmem_w(int rows, long long sectors) {
+  const int forced = pcs_internal::knobs().morton_w;
+  if ((forced == 4 || forced == 8 || forced == 16) && rows <= 32 * forced) return forced;
   int w = rows <= 128 ? 4 : rows <= 256 ? 8 : 16;
   if (w == 4 && rows > 64 && sectors <= 2 * 148) w = 8;
   return w;
