@@ -21,6 +21,10 @@ constexpr bool kSlotAsm = PCS_FULL_ASM != 0;
 #define PCS_FULL_CHAIN 4
 #endif
 constexpr int kChainLen = PCS_FULL_CHAIN;
+// most slots per thread that take the hand-spelled argmax chains
+#ifndef PCS_FULL_ARG_MAXP
+#define PCS_FULL_ARG_MAXP 8
+#endif
 
 // (best, bs) <- (bits, k) when bits > best: one 64-bit compare, three selects
 __device__ __forceinline__ void argmax_step(unsigned long long& best, int& bs,
@@ -93,13 +97,14 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
     // The update + running-argmax step of a slot, hand-spelled for 4 and 8
     // slots per thread (r02 s4, profiles/r02_full_slot_asm_ab.log: AFPS M=16
     // at 16K 1.31 -> 1.19 ms, M=64 at 32K 1.28 -> 1.20, M=16 at 8K 0.358 ->
-    // 0.337; with 16 slots the compiler's own schedule is 20% faster, with 1-2
-    // there is nothing to gain)
-    constexpr bool kAsm = REGC && kSlotAsm && (P == 4 || P == 8);
-    // (hand-spelled form: the running argmax as kChains independent chains
-    // over contiguous slot blocks, merged in slot order with the same strict
-    // compare, so the lowest slot still wins a tie)
-    constexpr int kChains = (kAsm && P > kChainLen) ? P / kChainLen : 1;
+    // 0.337; with 16 slots the compiler's own argmax is 18% faster and only
+    // the update part is taken, with 1-2 slots there is nothing to gain)
+    constexpr bool kAsm = REGC && kSlotAsm && (P == 4 || P == 8 || P == 16);
+    // 16 slots: only the update part (the hand-spelled argmax chains cost
+    // 18% there, the update part gains 1-3%)
+    constexpr bool kAsmUpd = kAsm;
+    constexpr bool kAsmArg = kAsm && P <= PCS_FULL_ARG_MAXP;
+    constexpr int kChains = (kAsmArg && P > kChainLen) ? P / kChainLen : 1;
     unsigned long long bestc[kChains];
     int bsc[kChains];
 #pragma unroll
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
       const double yy = REGC ? y[REGC ? k : 0] : gs.ys[min(j, n - 1)];
       const double zz = REGC ? z[REGC ? k : 0] : gs.zs[min(j, n - 1)];
       const double dist = dist2(xx, yy, zz, px, py, pz);
-      if constexpr (kAsm) {
+      if constexpr (kAsmUpd) {
         // one predicate per step, spelled out: the compiler's own form of
         // this loop re-derives the comparisons for the slot index (4 ISETP +
         // 3 SEL per slot) and counts writes with an add and a move
@@ -123,15 +128,17 @@ __global__ void __launch_bounds__(W * 32 * (W >= 8 ? 1 : (8 / W)))
         asm("{\n .reg .pred p;\n setp.le.f64 p, %2, %1;\n selp.f64 %1, %2, %1, p;\n"
             " @p add.u32 %0, %0, 1;\n}"
             : "+r"(writes), "+d"(d[k]) : "d"(dist));
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+      } else {
+        const bool lower = dist <= d[k];
+        writes += (lower && (REGC || ((vmask >> k) & 1u))) ? 1u : 0u;
+        d[k] = lower ? dist : d[k];
+      }
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
+      if constexpr (kAsmArg) {
         argmax_step(bestc[k * kChains / P], bsc[k * kChains / P], bits, k);
       } else {
         unsigned long long& best = bestc[0];
         int& bs = bsc[0];
-        const bool lower = dist <= d[k];
-        writes += (lower && (REGC || ((vmask >> k) & 1u))) ? 1u : 0u;
-        d[k] = lower ? dist : d[k];
-        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(d[k]));
         if (bits > best) {
           best = bits;
           bs = k;
