@@ -535,14 +535,26 @@ __global__ void __launch_bounds__(MAXT, MAXT == 128 ? 4 : 1) npdu_tmem_kernel(co
           dist[q] = dist2(static_cast<double>(xs[jc]), static_cast<double>(ys[jc]),
                           static_cast<double>(zs[jc]), px, py, pz);
         }
-        unsigned lmask = 0u;
+        if constexpr (RMAX <= 3) {
+          // window test, min-update and write count on one predicate, spelled
+          // out (r02 s4: windows of <= 3 rows 1-3% faster -- cfg3 0.078 ->
+          // 0.076 ms, 256x16K M=16 0.289 -> 0.282; 5-row windows 1% slower
+          // and kept on the compiler's form; profiles/r02_npdu_upd_asm_ab.log)
 #pragma unroll
-        for (int q = 0; q < RMAX; ++q) {
-          const bool lower = t0 + 32u * q < wlen && dist[q] <= dj[q];
-          lmask |= lower ? 1u << q : 0u;
-          dj[q] = lower ? dist[q] : dj[q];
+          for (int q = 0; q < RMAX; ++q)
+            asm("{\n .reg .pred p, w;\n setp.lt.u32 w, %3, %4;\n setp.le.and.f64 p, %2, %1, w;\n"
+                " selp.f64 %1, %2, %1, p;\n @p add.u32 %0, %0, 1;\n}"
+                : "+r"(writes), "+d"(dj[q]) : "d"(dist[q]), "r"(t0 + 32u * q), "r"(wlen));
+        } else {
+          unsigned lmask = 0u;
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q) {
+            const bool lower = t0 + 32u * q < wlen && dist[q] <= dj[q];
+            lmask |= lower ? 1u << q : 0u;
+            dj[q] = lower ? dist[q] : dj[q];
+          }
+          writes += __popc(lmask);
         }
-        writes += __popc(lmask);
         tm_store_rows<RMAX>(tm + 2 * r_lo, dj);
         uint32_t mh, ml = 0u, j;
         bool exact;
