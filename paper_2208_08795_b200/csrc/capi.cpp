@@ -358,19 +358,24 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
   char* base = static_cast<char*>(ws);
   if (e == cudaSuccess && ha->seeds)
     e = cudaMemcpyAsync(base + off_seed, ha->seeds, 8 * B, cudaMemcpyHostToDevice, copy);
+  const bool single = nch == 1;
   cudaEvent_t seeds_ready = ds.ev[kEvents - 1];  // the workspace (and seeds) exist
-  if (e == cudaSuccess) e = cudaEventRecord(seeds_ready, copy);
+  if (e == cudaSuccess && !single) e = cudaEventRecord(seeds_ready, copy);
   for (int i = 0; i < nch && e == cudaSuccess; ++i) {
     const int64_t b0 = bounds[i], b1 = bounds[i + 1], nb = b1 - b0;
     if (nb == 0) continue;
-    cudaStream_t w = work[i % kWorkers];
+    // one chunk: everything in order on the copy stream (no events, one
+    // synchronize); several: the chunk's work stream waits for its copy
+    cudaStream_t w = single ? copy : work[i % kWorkers];
     char* dx = base + off_xyz + cloud_bytes * b0;
     e = cudaMemcpyAsync(dx, static_cast<const char*>(ha->xyz) + cloud_bytes * b0,
                         cloud_bytes * nb, cudaMemcpyHostToDevice, copy);
-    cudaEvent_t ready = ds.ev[i];
-    if (e == cudaSuccess) e = cudaEventRecord(ready, copy);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(w, ready, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(w, seeds_ready, 0);
+    if (!single) {
+      cudaEvent_t ready = ds.ev[i];
+      if (e == cudaSuccess) e = cudaEventRecord(ready, copy);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(w, ready, 0);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(w, seeds_ready, 0);
+    }
     int32_t* dperm = reinterpret_cast<int32_t*>(base + off_perm) + N * b0;
     // the sort writes only the permutation; the sampler gathers through it
     if (e == cudaSuccess && sort_axis >= 0)
@@ -397,11 +402,11 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
     if (e == cudaSuccess && sort_axis >= 0 && out_perm)
       e = cudaMemcpyAsync(out_perm + N * b0, dperm, 4 * N * nb, cudaMemcpyDeviceToHost, w);
   }
-  for (int w = 0; w < kWorkers; ++w) {
+  for (int w = 0; w < kWorkers && !single; ++w) {
     const cudaError_t e2 = cudaStreamSynchronize(work[w]);
     if (e == cudaSuccess) e = e2;
   }
-  if (ws) cudaFreeAsync(ws, copy);  // every use above has completed
+  if (ws) cudaFreeAsync(ws, copy);  // every use above has completed (or precedes it on `copy`)
   {
     const cudaError_t e2 = cudaStreamSynchronize(copy);
     if (e == cudaSuccess) e = e2;
