@@ -313,6 +313,11 @@ int host_batch_device(const pcs_gpu_args* ha, int32_t sort_axis, int32_t* out_pe
     // 0.255 in four, cfg4 (50 MB) best at 8)
     const int64_t by_size = static_cast<int64_t>((cloud_bytes * B) / (size_t(3) << 19));
     int64_t def = std::max<int64_t>(1, std::min<int64_t>(8, by_size));
+    // inputs beyond ~50 MB keep chunks of ~6 MiB, up to 16 (r02 s4,
+    // tools/e2e_parts.py: 256 x 32K (100 MB) NPDU 2.43 ms in 8 chunks vs 2.34
+    // in 12-16, AFPS M=256 2.29 vs 2.17; cfg4 (50 MB) stays best at 8)
+    if (def == 8)
+      def = std::max<int64_t>(8, std::min<int64_t>(16, static_cast<int64_t>((cloud_bytes * B) / (size_t(6) << 20))));
     // Compute-heavy calls with few sectors (many reference distance
     // evaluations per input point, about one wave of sectors: full-window
     // FPS / AFPS M=1) are bound by their kernels' serial iteration chains,
