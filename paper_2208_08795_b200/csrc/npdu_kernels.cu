@@ -509,10 +509,14 @@ __global__ void __launch_bounds__(MAXT, MAXT == 128 ? 4 : 1) npdu_tmem_kernel(co
     };
     int marked = 0;  // outputs [0, marked) are in the bitmap
     unsigned writes = 0;
-    // blocks of 32 outputs: the inner loop has no flush test
+    // blocks of 32 outputs: the inner loop has no flush test; windows of
+    // <= 3 rows run it unrolled by two (r02 s4: cfg3 0.076 -> 0.074 ms,
+    // 256x16K M=16 0.281 -> 0.276; 5-row windows 0.7% slower, not unrolled;
+    // profiles/r02_npdu_upd_asm_ab.log)
+    constexpr int kIterUnroll = RMAX <= 3 ? 2 : 1;
     for (int blk = 0; blk < g.quota; blk += 32) {
       const int it_end = min(blk + 32, g.quota);
-#pragma unroll 1
+#pragma unroll kIterUnroll
       for (int it = blk > 0 ? blk : 1; it < it_end; ++it) {
         const double px = static_cast<double>(xs[cur]), py = static_cast<double>(ys[cur]),
                      pz = static_cast<double>(zs[cur]);
